@@ -1,0 +1,71 @@
+"""Helpers shared by the parity tests: run the oracle / load golden vectors."""
+
+from __future__ import annotations
+
+import json
+from pathlib import Path
+
+import numpy as np
+
+import cases
+from oracle import codec_oracle as orc
+
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def oracle_run(x, scheme, group, thr):
+    """Oracle compress+decompress -> (normalized dict, dequant) or error name."""
+    try:
+        ct = orc.compress(x, scheme, group, thr)
+    except orc.OracleError as exc:
+        return exc.kind, None
+    deq = orc.decompress(ct)
+    norm = cases.normalized(
+        None if scheme == cases.MASK else ct.scales, ct.offsets,
+        None if scheme == cases.MASK else ct.codes,
+        ct.outlier_idx, ct.outlier_val, ct.mask_bits)
+    return norm, deq
+
+
+def load_small():
+    """{name: {"error": str} | {key: array, "dequant": array}} from small_golden.npz."""
+    z = np.load(GOLDEN / "small_golden.npz")
+    out = {str(n): {} for n in z["__names__"]}
+    for key in z.files:
+        if key == "__names__":
+            continue
+        name, field = key.split("/", 1)
+        out[name][field] = z[key]
+    for name, d in out.items():
+        if "error" in d:
+            d["error"] = str(d["error"])
+    return out
+
+
+def load_digests():
+    return json.loads((GOLDEN / "digests.json").read_text())
+
+
+def small_inputs():
+    return {name: (x, s, g, t) for name, x, s, g, t in
+            cases.kat_cases() + cases.random_cases() + cases.tie_family_cases()}
+
+
+def assert_matches_golden(name, golden, norm, deq):
+    if "error" in golden:
+        assert norm == golden["error"], f"{name}: expected {golden['error']}, got {norm!r}"
+        return
+    assert not isinstance(norm, str), f"{name}: unexpected error {norm}"
+    for key in ("scales", "offsets", "codes", "idx", "vals", "mask"):
+        want = golden.get(key)
+        got = norm[key]
+        if want is None:
+            assert got is None or got.size == 0, f"{name}/{key}: expected none"
+        else:
+            assert got is not None, f"{name}/{key}: missing"
+            np.testing.assert_array_equal(np.asarray(got), want, err_msg=f"{name}/{key}")
+    want = np.ascontiguousarray(golden["dequant"])
+    got = np.ascontiguousarray(np.asarray(deq))
+    assert got.shape == want.shape and got.dtype == want.dtype, f"{name}/dequant: {got.shape}/{got.dtype}"
+    # bitwise, so -0.0 vs +0.0 would be caught too
+    np.testing.assert_array_equal(got.view(np.uint8), want.view(np.uint8), err_msg=f"{name}/dequant")
