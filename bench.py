@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the activation-compressor hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1], the configuration the metric is quoted on):
+the nine saved activations of one GPT-345M transformer block at batch 8,
+seq 1024, bf16 (h=1024, 16 heads, FFN 4096, explicit attention), each routed
+through ``scheme_for(kind)`` (codec.py:72-82).  One step = compress all nine in
+forward order, then decompress all nine in backward order to bf16 (masks to
+bytes) -- what one block does per training step.  Synthetic data (no dataset
+download), generated on the device.  The step's working set (~0.9 GB in,
+~0.9 GB out) is far larger than the 126 MB L2, so no flush is needed.
+
+value = algorithmic bytes (compress: N*s_in + payload; decompress: payload +
+N*s_out) of all ranks / max-over-ranks device time, GB/s.
+e2e   = the same metric through the C-ABI with host buffers: pinned H2D of
+the step's inputs, compress, decompress, D2H of the reconstructions.
+``--impl reference`` times the reference algorithm (the numpy oracle port,
+oracle/codec_oracle.py) on all host cores on a bounded row-sample of the same
+workload, as the driver's reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "compress+decompress GB/s per B200 (% of HBM peak); training tokens/sec at 1/2/4/8 GPU"
+UNIT = "GB/s"
+WORKLOAD = "gpt345m-block-activations"
+CONFIG = {"workload": WORKLOAD, "model_shape": "GPT-345M block (h=1024, 16 heads, ffn 4096)",
+          "batch": 8, "seq_len": 1024, "tensors": 9, "input_dtype": "bf16",
+          "output_dtype": "bf16 (masks u8)", "l2": "working set ~1.8 GB/step >> 126 MB L2, no flush"}
+SAMPLE_DIV = 32  # CPU arms process 1/32 of each tensor's rows per step
+
+
+# ---------------------------------------------------------------------------
+# CPU arms (reference algorithm = oracle port; test infrastructure)
+# ---------------------------------------------------------------------------
+def _cpu_sample(seed: int):
+    """Row-sample of the block's nine tensors as numpy arrays (same distributions)."""
+    import numpy as np
+    from paper_2508_00806_b200.workload import gpt_block_ops
+    rng = np.random.default_rng(seed)
+    out = []
+    for op in gpt_block_ops():
+        rows = max(8, op.rows // SAMPLE_DIV)
+        kind = op.kind.value
+        if kind == "dropout_mask":
+            x = (rng.random((rows, op.cols)) < 0.9).astype(np.uint8)
+        elif kind == "score":
+            x = rng.normal(size=(rows, op.cols)).astype(np.float32) * 3
+        elif kind == "softmax":
+            s = rng.normal(size=(rows, op.cols)) * 3
+            e = np.exp(s - s.max(axis=1, keepdims=True))
+            x = (e / e.sum(axis=1, keepdims=True)).astype(np.float32)
+        else:
+            x = rng.normal(size=(rows, op.cols)).astype(np.float32)
+            hot = rng.choice(op.cols, max(1, op.cols // 100), replace=False)
+            x[:, hot] *= 30.0
+        out.append((kind, x))
+    return out
+
+
+def _cpu_work(args):
+    """One process: compress+decompress its sample with the oracle; (bytes, seconds)."""
+    seed, reps = args
+    from oracle import codec_oracle as orc
+    sample = _cpu_sample(seed)
+    total = 0
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        for kind, x in sample:
+            scheme, group = orc.SCHEME_OF_KIND[kind]
+            ct = orc.compress(x, scheme, group)
+            orc.decompress(ct)
+            n = x.size
+            pay = ct.payload_bytes()
+            s_in = 1 if scheme == orc.BIT_MASK else 2
+            total += (n * s_in + pay) + (pay + n * s_in)
+    return total, time.perf_counter() - t0
+
+
+def cpu_measure(procs: int, reps: int = 1):
+    """Aggregate GB/s of `procs` independent processes (one core each)."""
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+    ctx = mp.get_context("fork")
+    with ctx.Pool(procs) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_cpu_work, [(1000 + i, reps) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    total = sum(b for b, _ in res)
+    return total / wall / 1e9, wall, total
+
+
+def host_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, rank: int) -> None:
+    if rank != 0:
+        return
+    procs = host_cores()
+    sample = (f"1/{SAMPLE_DIV} of the rows of each of the 9 block tensors per process per step, "
+              f"{procs} processes (one per host core), numpy oracle port of codec.py")
+    for _ in range(args.warmup):
+        cpu_measure(procs)
+    times, vals = [], []
+    for _ in range(args.steps):
+        v, wall, _ = cpu_measure(procs)
+        vals.append(v)
+        times.append(wall)
+    value = statistics.median(vals)
+    line = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(1e3 * statistics.median(times), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f16 codes from f32 input (CPU)",
+            "data": "synthetic", "config": CONFIG,
+            "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": procs,
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (NVML, polled during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.ok = [], set(), False
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            self.ok = False
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.002)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                    "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def measured_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic(kernel_key: str):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = ROOT / "profiles" / "ncu_summary.json"
+    try:
+        d = json.loads(p.read_text())
+        return d["kernels"][kernel_key]["dram_bytes_per_launch"]
+    except Exception:
+        return None
+
+
+def run_ours(args, rank: int, world: int, local_rank: int) -> None:
+    import torch
+    import torch.distributed as dist
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200 import _lib
+    from paper_2508_00806_b200.slots import CodecSlot
+    from paper_2508_00806_b200.workload import gpt_block_ops, synth_activation
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    stream = torch.cuda.current_stream(dev)
+    sptr = stream.cuda_stream
+    ops = gpt_block_ops()
+    xs, slots, outs = [], [], []
+    for op in ops:
+        x = synth_activation(op, seed=rank + 1, device=dev)
+        spec = adc.scheme_for(op.kind)
+        in_dt = torch.bool if x.dtype == torch.bool else x.dtype
+        k_cap = None
+        if spec.scheme is adc.Scheme.OUTLIER_SEPARATED:
+            k = adc.compress(x, spec).outlier_count        # "tracking" pass sizes the side buffer
+            k_cap = max(16, 2 * k)
+        slot = CodecSlot(op.rows, op.cols, spec, in_dt,
+                         torch.uint8 if x.dtype == torch.bool else torch.bfloat16,
+                         k_cap=k_cap, device=dev)
+        xs.append(x)
+        slots.append(slot)
+        outs.append(torch.empty((op.rows, op.cols), dtype=slot.out_dtype, device=dev))
+    x_ptrs = [x.data_ptr() for x in xs]
+    y_ptrs = [y.data_ptr() for y in outs]
+
+    def step(ev=None):
+        for i, s in enumerate(slots):
+            if ev is not None:
+                ev[2 * i].record(stream)
+            s.compress_ptr(x_ptrs[i], sptr)
+            if ev is not None:
+                ev[2 * i + 1].record(stream)
+        for i in reversed(range(len(slots))):
+            if ev is not None:
+                ev[2 * len(slots) + 2 * i].record(stream)
+            slots[i].decompress_ptr(y_ptrs[i], sptr)
+            if ev is not None:
+                ev[2 * len(slots) + 2 * i + 1].record(stream)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    status_err = int(slots[0].status[0].item())
+    ks = [int(s.k_status[1].item()) if s.k_cap else 0 for s in slots]
+    bytes_c = [s.algorithmic_bytes(k)[0] for s, k in zip(slots, ks)]
+    bytes_d = [s.algorithmic_bytes(k)[1] for s, k in zip(slots, ks)]
+    bytes_step = sum(bytes_c) + sum(bytes_d)
+
+    # ---- timed region: exactly K steps, per-op events on the launching stream
+    n_ev = 4 * len(slots)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_ev)] for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = _lib.lib().adc_kernel_launches()
+    with ClockSampler(local_rank) as clocks:
+        t_start.record(stream)
+        for k in range(args.steps):
+            step(evs[k])
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.lib().adc_kernel_launches() - launches0
+    if world > 1:
+        dist.barrier()
+    ms = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = world * bytes_step * args.steps / (ms_max / 1e3) / 1e9
+
+    # per-op averages (compress / decompress) over the timed steps
+    per_op = []
+    for i, (op, s) in enumerate(zip(ops, slots)):
+        c = statistics.mean(e[2 * i].elapsed_time(e[2 * i + 1]) for e in evs)
+        d = statistics.mean(e[2 * len(slots) + 2 * i].elapsed_time(e[2 * len(slots) + 2 * i + 1]) for e in evs)
+        per_op.append({"op": op.name, "scheme": s.scheme.name, "shape": [op.rows, op.cols],
+                       "k": ks[i], "compress_us": round(c * 1e3, 2), "decompress_us": round(d * 1e3, 2),
+                       "compress_gbs": round(bytes_c[i] / c / 1e6, 1),
+                       "decompress_gbs": round(bytes_d[i] / d / 1e6, 1)})
+    peak, peak_src = measured_peak()
+    # dominant single-kernel call: the largest-time call among those that are one launch
+    single = [(p["compress_us"], p, "compress") for p in per_op if p["scheme"] in ("ASYMMETRIC_GROUP", "BIT_MASK", "SYMMETRIC_GROUP")]
+    single += [(p["decompress_us"], p, "decompress") for p in per_op if p["scheme"] != "OUTLIER_SEPARATED"]
+    _, dom, phase = max(single, key=lambda t: t[0])
+    dom_i = [p["op"] for p in per_op].index(dom["op"])
+    dom_bytes = bytes_c[dom_i] if phase == "compress" else bytes_d[dom_i]
+    dom_us = dom["compress_us"] if phase == "compress" else dom["decompress_us"]
+    achieved = dom_bytes / (dom_us * 1e-6) / 1e9
+    kernel_key = f"{dom['op']}/{phase}"
+    step_ms = ms / args.steps
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": ncu_traffic(kernel_key),
+                "kernel": kernel_key, "algorithmic_bytes_per_launch": dom_bytes,
+                "peak_source": f"{peak_src} hbm_gbs (MEASURED_PEAKS.json copy bandwidth)",
+                "share_of_step": round(dom_us / 1e3 / step_ms, 4),
+                "step_frac": round(value / world / peak, 4)}
+
+    # ---- e2e through the C-ABI with host buffers
+    e2e_steps = max(1, min(args.steps, 5))
+    hx = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in xs]
+    for h, x in zip(hx, xs):
+        h.copy_(x)
+    hy = [torch.empty(y.shape, dtype=y.dtype, pin_memory=True) for y in outs]
+    h2d = sum(h.numel() * h.element_size() for h in hx)
+    d2h = sum(h.numel() * h.element_size() for h in hy)
+
+    def e2e_step():
+        for h, x in zip(hx, xs):
+            x.copy_(h, non_blocking=True)
+        step()
+        for h, y in zip(hy, outs):
+            h.copy_(y, non_blocking=True)
+
+    e2e_step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        e2e_step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
+    e2e_value = world * bytes_step * e2e_steps / (float(e_ms.item()) / 1e3) / 1e9
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        procs = host_cores()
+        v, wall, tot = cpu_measure(procs, reps=args.cpu_reps)
+        cpu = {"value": round(v, 4), "unit": UNIT, "cores": procs, "kind": "port",
+               "sample": f"1/{SAMPLE_DIV} of the rows of each of the 9 block tensors x {args.cpu_reps} "
+                         f"per process, {procs} processes, numpy oracle port; {wall:.1f} s wall, "
+                         f"{tot / 1e9:.2f} GB algorithmic"}
+    if rank == 0:
+        line = {"metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (device-generated, GPT-345M-shaped activations)",
+                "config": dict(CONFIG, parallelism=f"replicas x{world} (rank-local codec)"),
+                "bytes_per_step_per_gpu": bytes_step,
+                "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
+                        "d2h_bytes_per_step": d2h, "steps": e2e_steps},
+                "clocks": clocks.summary(), "gpu_launches": int(launches),
+                "device_error_word": status_err, "per_op": per_op}
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * adacc.h -- C-ABI of the B200 activation-compressor path (Adacc, arXiv 2508.00806).
+ *
+ * This is the drop-in boundary for the reference's codec module
+ * (/root/reference/pkg/src/actplan/codec.py).  Every entry point below names
+ * the reference function it replaces.  Conventions:
+ *
+ *   - All array arguments are DEVICE pointers owned by the caller; the library
+ *     never allocates.  `workspace` is caller-owned scratch of
+ *     adc_workspace_bytes() bytes (256-byte aligned).
+ *   - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t
+ *     passed as void*; NULL = legacy default stream).  Return value is a
+ *     synchronous status: ADC_OK, ADC_EINVAL (argument validation, the
+ *     reference's ValidationError), ADC_EWORKSPACE, or ADC_ECUDA (launch
+ *     failure; adc_last_error() has the text).
+ *   - Data-dependent failures are OR-ed into the device word `err_word` as
+ *     ADC_ERR_* bits (never cleared by the library): non-finite after the
+ *     float16 cast (NonFiniteInputError, codec.py:167-170), more than half the
+ *     channels flagged (TooManyOutliersError, codec.py:324-327), k above the
+ *     caller's side-buffer capacity, or a non-binary mask (NonBinaryMaskError,
+ *     codec.py:355-357).  Outputs are unspecified when a bit is set.
+ *   - Inputs are C-contiguous (rows, cols) matrices, channel = last dim
+ *     (rows = product of the leading dims, codec.py:161-162).  Input dtypes:
+ *     ADC_F32, ADC_BF16, ADC_F16 (all cast to float16 RNE first, codec.py:158);
+ *     masks additionally ADC_U8 (bytes 0/1, bool tensors).
+ *   - Payload layout is the reference's (codec.py:85-145): float16 scales
+ *     (and offsets) as uint16 bit patterns, one per group; packed int4 codes,
+ *     earlier element in the low nibble, row-major groups over the flattened
+ *     tensor, COLUMN-major for group_size == ADC_PER_CHANNEL; outlier indices
+ *     ascending uint32; outlier values float16 laid out (k, rows).
+ *   - Reentrant: concurrent calls are safe with distinct buffers/workspaces.
+ */
+#ifndef ADACC_H
+#define ADACC_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADC_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define ADC_API __attribute__((visibility("default")))
+#else
+#define ADC_API
+#endif
+
+/* Scheme ids == reference Scheme IntEnum == ADC1 scheme byte (codec.py:56-60). */
+#define ADC_SYMMETRIC_GROUP 0
+#define ADC_ASYMMETRIC_GROUP 1
+#define ADC_OUTLIER_SEPARATED 2
+#define ADC_BIT_MASK 3
+
+/* group_size sentinel: one group per channel (codec.py:45). */
+#define ADC_PER_CHANNEL 0
+
+/* element dtypes */
+#define ADC_F32 0
+#define ADC_BF16 1
+#define ADC_F16 2
+#define ADC_U8 3
+
+/* synchronous status codes */
+#define ADC_OK 0
+#define ADC_EINVAL (-1)
+#define ADC_ECUDA (-2)
+#define ADC_EWORKSPACE (-3)
+
+/* device error-word bits */
+#define ADC_ERR_NONFINITE 1u
+#define ADC_ERR_TOO_MANY_OUTLIERS 2u
+#define ADC_ERR_K_CAP 4u
+#define ADC_ERR_NONBINARY 8u
+
+/* Library / ABI identification. */
+ADC_API const char *adc_version(void);
+ADC_API int adc_abi_version(void);
+/* Text of the last failing call on this host thread ("" if none). */
+ADC_API const char *adc_last_error(void);
+/* Number of CUDA kernels launched by this library since load (all threads). */
+ADC_API unsigned long long adc_kernel_launches(void);
+
+/*
+ * Closed-form payload size; replaces packed_payload_bytes (codec.py:133-145).
+ * Writes the group count, packed-code bytes and total payload bytes (any
+ * output pointer may be NULL).  Host-only, no CUDA.
+ */
+ADC_API int adc_payload_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size,
+                      int64_t outlier_count, int64_t *n_groups, int64_t *code_bytes,
+                      int64_t *payload_bytes);
+
+/* Scratch bytes adc_compress / adc_detect_outliers need for this shape. */
+ADC_API size_t adc_workspace_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size);
+
+/*
+ * Compress one activation matrix; replaces compress (codec.py:381-389) and
+ * thereby quantize_symmetric (:245), quantize_asymmetric (:255),
+ * compress_outlier_separated (:308) and pack_bitmask (:344).
+ *
+ *   codes       ceil(rows*cols/2) bytes (BIT_MASK: ceil(rows*cols/8) mask bytes)
+ *   scales      n_groups uint16 (f16 bits); unused for BIT_MASK
+ *   offsets     n_groups uint16; ASYMMETRIC_GROUP only
+ *   outlier_idx k_cap uint32, outlier_val k_cap*rows uint16, k_out one int32:
+ *               OUTLIER_SEPARATED only.  k_out receives k even when k > k_cap
+ *               (then ADC_ERR_K_CAP is raised and idx/val are incomplete).
+ *   z_threshold OUTLIER_SEPARATED z-score threshold (codec.py:43, strict >).
+ */
+ADC_API int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t cols,
+                 int64_t group_size, double z_threshold, int64_t k_cap,
+                 uint8_t *codes, uint16_t *scales, uint16_t *offsets,
+                 uint32_t *outlier_idx, uint16_t *outlier_val, int32_t *k_out,
+                 uint32_t *err_word, void *workspace, size_t workspace_bytes, void *stream);
+
+/*
+ * Decompress; replaces decompress (codec.py:392-395) = dequantize (:261-286)
+ * / unpack_bitmask (:372-378).  `y` is (rows, cols) of out_dtype: ADC_F32
+ * reproduces the reference output bit-exactly; ADC_BF16 / ADC_F16 are the
+ * float32 result rounded RNE (training mode).  BIT_MASK writes 0/1 bytes
+ * (out_dtype ADC_U8).  `k_dev` is the device outlier count written by
+ * adc_compress; at most k_cap outlier columns are scattered.
+ */
+ADC_API int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
+                   const uint16_t *offsets, const uint32_t *outlier_idx,
+                   const uint16_t *outlier_val, const int32_t *k_dev, int64_t k_cap,
+                   int64_t rows, int64_t cols, int64_t group_size, void *y, int out_dtype,
+                   void *stream);
+
+/* Column sums of |f16(x)| in float64; replaces channel_abs_sums (codec.py:289-291). */
+ADC_API int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols,
+                         double *sums, uint32_t *err_word, void *workspace,
+                         size_t workspace_bytes, void *stream);
+
+/*
+ * Outlier channel indices; replaces detect_outlier_channels (codec.py:294-305).
+ * Writes ascending indices (up to k_cap) and k.
+ */
+ADC_API int adc_detect_outliers(const void *x, int in_dtype, int64_t rows, int64_t cols,
+                        double z_threshold, int64_t k_cap, uint32_t *outlier_idx,
+                        int32_t *k_out, uint32_t *err_word, void *workspace,
+                        size_t workspace_bytes, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADACC_H */

@@ -1,0 +1,79 @@
+"""ctypes binding of the C-ABI library ``_lib/libadacc.so`` (include/adacc.h).
+
+The product path has no CPU fallback: if the library is missing this module
+raises on first use instead of silently degrading.  Loading the library does
+not touch the GPU, so the symbol table can be checked on a CPU-only host.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libadacc.so"
+
+# enum mirrors of include/adacc.h
+SYMMETRIC_GROUP, ASYMMETRIC_GROUP, OUTLIER_SEPARATED, BIT_MASK = 0, 1, 2, 3
+PER_CHANNEL = 0
+F32, BF16, F16, U8 = 0, 1, 2, 3
+OK, EINVAL, ECUDA, EWORKSPACE = 0, -1, -2, -3
+
+_i64, _vp, _sz = C.c_int64, C.c_void_p, C.c_size_t
+_P64 = C.POINTER(C.c_int64)
+
+SIGNATURES = {
+    "adc_version": (C.c_char_p, []),
+    "adc_abi_version": (C.c_int, []),
+    "adc_last_error": (C.c_char_p, []),
+    "adc_kernel_launches": (C.c_ulonglong, []),
+    "adc_payload_bytes": (C.c_int, [C.c_int, _i64, _i64, _i64, _i64, _P64, _P64, _P64]),
+    "adc_workspace_bytes": (_sz, [C.c_int, _i64, _i64, _i64]),
+    "adc_compress": (C.c_int, [C.c_int, _vp, C.c_int, _i64, _i64, _i64, C.c_double, _i64,
+                               _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "adc_decompress": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64,
+                                 _i64, _vp, C.c_int, _vp]),
+    "adc_channel_abs_sums": (C.c_int, [_vp, C.c_int, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "adc_detect_outliers": (C.c_int, [_vp, C.c_int, _i64, _i64, C.c_double, _i64, _vp, _vp,
+                                      _vp, _vp, _sz, _vp]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class LibraryMissingError(RuntimeError):
+    """libadacc.so is not built: there is deliberately no fallback path."""
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise LibraryMissingError(
+                    f"{LIB_PATH} not found; build it with `python -m paper_2508_00806_b200.build` "
+                    "(the compressor has no CPU fallback)")
+            handle = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    return lib().adc_last_error().decode()
+
+
+def check(status: int, what: str) -> None:
+    if status == OK:
+        return
+    from .errors import CudaError, ValidationError
+    msg = f"{what}: {last_error()}"
+    if status == EINVAL:
+        raise ValidationError(msg)
+    raise CudaError(msg)

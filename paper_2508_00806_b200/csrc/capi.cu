@@ -1,0 +1,244 @@
+// C-ABI entry points (include/adacc.h): argument validation, workspace
+// carving and kernel dispatch.  No allocation, no synchronisation.
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "common.cuh"
+#include "launch.h"
+
+namespace adc {
+
+static thread_local std::string g_last_error;
+static std::atomic<unsigned long long> g_launches{0};
+
+void note_launches(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
+
+static int fail(int code, const char *msg) {
+  g_last_error = msg;
+  return code;
+}
+
+static int check_launch(const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+    return ADC_ECUDA;
+  }
+  g_last_error.clear();
+  return ADC_OK;
+}
+
+static int sm_count() {
+  static int cached[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  if (!cached[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+      n = 148;
+    cached[dev] = n;
+  }
+  return cached[dev];
+}
+
+static inline size_t up256(size_t v) { return (v + 255) & ~size_t(255); }
+
+static int64_t leaf_capacity(int64_t cols) { return cols / 32 + 8; }
+
+size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
+  char *p = static_cast<char *>(base);
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char *r = p ? p + off : nullptr;
+    off += up256(bytes);
+    return r;
+  };
+  Workspace w;
+  w.colsum = reinterpret_cast<double *>(take(sizeof(double) * cols));
+  w.colmax = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
+  w.flag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
+  w.rank = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * cols));
+  w.leaf = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * leaf_capacity(cols)));
+  w.leafsum = reinterpret_cast<double *>(take(sizeof(double) * leaf_capacity(cols)));
+  w.misc = reinterpret_cast<uint32_t *>(take(64));
+  w.bytes = off;
+  if (ws) *ws = w;
+  return off;
+}
+
+static bool valid_float_dtype(int dt) { return dt == ADC_F32 || dt == ADC_BF16 || dt == ADC_F16; }
+
+}  // namespace adc
+
+using namespace adc;
+
+extern "C" {
+
+const char *adc_version(void) { return "adacc-b200 0.1.0 (sm_100a)"; }
+
+int adc_abi_version(void) { return ADC_ABI_VERSION; }
+
+const char *adc_last_error(void) { return g_last_error.c_str(); }
+
+unsigned long long adc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int adc_payload_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size,
+                      int64_t outlier_count, int64_t *n_groups, int64_t *code_bytes,
+                      int64_t *payload_bytes) {
+  if (scheme < 0 || scheme > 3) return fail(ADC_EINVAL, "unknown scheme");
+  if (rows < 1 || cols < 1) return fail(ADC_EINVAL, "shape must be at least 1x1");
+  const int64_t n = rows * cols;
+  int64_t groups = 0, codes = 0, total = 0;
+  if (scheme == ADC_BIT_MASK) {
+    codes = (n + 7) / 8;
+    total = codes;
+  } else {
+    if (group_size < 0) return fail(ADC_EINVAL, "group_size must be positive or PER_CHANNEL");
+    groups = group_size == ADC_PER_CHANNEL ? cols : (n + group_size - 1) / group_size;
+    codes = (n + 1) / 2;
+    total = (scheme == ADC_ASYMMETRIC_GROUP ? 4 : 2) * groups + codes;
+    if (scheme == ADC_OUTLIER_SEPARATED) total += outlier_count * (4 + 2 * rows);
+  }
+  if (n_groups) *n_groups = groups;
+  if (code_bytes) *code_bytes = codes;
+  if (payload_bytes) *payload_bytes = total;
+  return ADC_OK;
+}
+
+size_t adc_workspace_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size) {
+  (void)scheme;
+  (void)rows;
+  (void)group_size;
+  if (cols < 1) cols = 1;
+  return workspace_layout(cols, nullptr, nullptr);
+}
+
+int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t cols,
+                 int64_t group_size, double z_threshold, int64_t k_cap, uint8_t *codes,
+                 uint16_t *scales, uint16_t *offsets, uint32_t *outlier_idx, uint16_t *outlier_val,
+                 int32_t *k_out, uint32_t *err_word, void *workspace, size_t workspace_bytes,
+                 void *stream) {
+  if (scheme < 0 || scheme > 3) return fail(ADC_EINVAL, "unknown scheme");
+  if (rows < 1 || cols < 1) return fail(ADC_EINVAL, "activation matrix must have at least one element");
+  if (!x || !codes) return fail(ADC_EINVAL, "null input or code buffer");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  const int64_t n = rows * cols;
+  if (scheme == ADC_BIT_MASK) {
+    if (!(valid_float_dtype(in_dtype) || in_dtype == ADC_U8)) return fail(ADC_EINVAL, "bad mask dtype");
+    if (launch_mask_pack(c, x, in_dtype, n, codes, err_word)) return fail(ADC_EINVAL, "mask dispatch");
+    return check_launch("mask_pack");
+  }
+  if (!valid_float_dtype(in_dtype)) return fail(ADC_EINVAL, "activation dtype must be f32, bf16 or f16");
+  if (group_size != ADC_PER_CHANNEL && group_size < 1)
+    return fail(ADC_EINVAL, "group_size must be positive or PER_CHANNEL");
+  if (!scales) return fail(ADC_EINVAL, "null scale buffer");
+  if (scheme == ADC_ASYMMETRIC_GROUP && !offsets) return fail(ADC_EINVAL, "null offset buffer");
+  const bool asym = scheme == ADC_ASYMMETRIC_GROUP;
+  const bool pc = group_size == ADC_PER_CHANNEL;
+  int rc = 0;
+  if (scheme == ADC_OUTLIER_SEPARATED) {
+    if (!k_out || (k_cap > 0 && (!outlier_idx || !outlier_val)))
+      return fail(ADC_EINVAL, "outlier buffers required");
+    if (!workspace || workspace_bytes < workspace_layout(cols, nullptr, nullptr))
+      return fail(ADC_EWORKSPACE, "workspace too small");
+    Workspace ws;
+    workspace_layout(cols, &ws, workspace);
+    if (cudaMemsetAsync(ws.flag, 0, static_cast<size_t>(cols) + 8, c.stream) != cudaSuccess)
+      return check_launch("memset");
+    rc |= launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
+    rc |= launch_outlier_stats(c, rows, cols, z_threshold, k_cap, ws, outlier_idx, k_out, err_word,
+                               true);
+    rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag, ws.rank,
+                                outlier_idx, k_out, outlier_val, k_cap, codes, scales, nullptr,
+                                err_word);
+    if (rc) return fail(ADC_EINVAL, "outlier dispatch");
+    return check_launch("outlier_separated");
+  }
+  if (pc && !asym && channel_fast_ok(x, rows, cols, codes, scales)) {
+    if (!workspace || workspace_bytes < workspace_layout(cols, nullptr, nullptr))
+      return fail(ADC_EWORKSPACE, "workspace too small");
+    Workspace ws;
+    workspace_layout(cols, &ws, workspace);
+    if (launch_channel_compress(c, x, in_dtype, rows, cols, ws, codes, scales, err_word))
+      return fail(ADC_EINVAL, "channel dispatch");
+    return check_launch("per_channel");
+  }
+  rc = launch_group_compress(c, x, in_dtype, rows, cols, group_size, asym, nullptr, nullptr,
+                             nullptr, nullptr, nullptr, 0, codes, scales, offsets, err_word);
+  if (rc) return fail(ADC_EINVAL, "group dispatch");
+  return check_launch("group_quant");
+}
+
+int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
+                   const uint16_t *offsets, const uint32_t *outlier_idx,
+                   const uint16_t *outlier_val, const int32_t *k_dev, int64_t k_cap, int64_t rows,
+                   int64_t cols, int64_t group_size, void *y, int out_dtype, void *stream) {
+  if (scheme < 0 || scheme > 3) return fail(ADC_EINVAL, "unknown scheme");
+  if (rows < 1 || cols < 1) return fail(ADC_EINVAL, "bad shape");
+  if (!codes || !y) return fail(ADC_EINVAL, "null buffer");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  const int64_t n = rows * cols;
+  if (scheme == ADC_BIT_MASK) {
+    if (out_dtype != ADC_U8) return fail(ADC_EINVAL, "masks decompress to u8");
+    launch_mask_unpack(c, codes, n, static_cast<uint8_t *>(y));
+    return check_launch("mask_unpack");
+  }
+  if (!valid_float_dtype(out_dtype)) return fail(ADC_EINVAL, "output dtype must be f32, bf16 or f16");
+  if (group_size != ADC_PER_CHANNEL && group_size < 1) return fail(ADC_EINVAL, "bad group_size");
+  if (!scales) return fail(ADC_EINVAL, "null scales");
+  const bool asym = scheme == ADC_ASYMMETRIC_GROUP;
+  if (asym && !offsets) return fail(ADC_EINVAL, "null offsets");
+  const bool pc = group_size == ADC_PER_CHANNEL;
+  int rc = 0;
+  if (pc && !asym && channel_fast_ok(y, rows, cols, codes, scales) &&
+      reinterpret_cast<uintptr_t>(y) % 16 == 0) {
+    rc = launch_channel_decompress(c, codes, scales, rows, cols, y, out_dtype);
+  } else {
+    rc = launch_group_decompress(c, codes, scales, asym ? offsets : nullptr, rows, cols, group_size,
+                                 asym, y, out_dtype);
+  }
+  if (rc) return fail(ADC_EINVAL, "decompress dispatch");
+  if (scheme == ADC_OUTLIER_SEPARATED && k_cap > 0) {
+    if (!outlier_idx || !outlier_val || !k_dev) return fail(ADC_EINVAL, "outlier buffers required");
+    launch_outlier_scatter(c, outlier_idx, outlier_val, k_dev, k_cap, rows, cols, y, out_dtype);
+  }
+  return check_launch("decompress");
+}
+
+int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols, double *sums,
+                         uint32_t *err_word, void *workspace, size_t workspace_bytes,
+                         void *stream) {
+  if (rows < 1 || cols < 1 || !x || !sums) return fail(ADC_EINVAL, "bad arguments");
+  if (!valid_float_dtype(in_dtype)) return fail(ADC_EINVAL, "bad dtype");
+  if (!workspace || workspace_bytes < workspace_layout(cols, nullptr, nullptr))
+    return fail(ADC_EWORKSPACE, "workspace too small");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  Workspace ws;
+  workspace_layout(cols, &ws, workspace);
+  launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
+  launch_copy_sums(c, ws, sums, cols);
+  return check_launch("channel_abs_sums");
+}
+
+int adc_detect_outliers(const void *x, int in_dtype, int64_t rows, int64_t cols,
+                        double z_threshold, int64_t k_cap, uint32_t *outlier_idx, int32_t *k_out,
+                        uint32_t *err_word, void *workspace, size_t workspace_bytes,
+                        void *stream) {
+  if (rows < 1 || cols < 1 || !x || !k_out) return fail(ADC_EINVAL, "bad arguments");
+  if (k_cap > 0 && !outlier_idx) return fail(ADC_EINVAL, "null index buffer");
+  if (!valid_float_dtype(in_dtype)) return fail(ADC_EINVAL, "bad dtype");
+  if (!workspace || workspace_bytes < workspace_layout(cols, nullptr, nullptr))
+    return fail(ADC_EWORKSPACE, "workspace too small");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  Workspace ws;
+  workspace_layout(cols, &ws, workspace);
+  if (cudaMemsetAsync(ws.flag, 0, static_cast<size_t>(cols) + 8, c.stream) != cudaSuccess)
+    return check_launch("memset");
+  launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
+  launch_outlier_stats(c, rows, cols, z_threshold, k_cap, ws, outlier_idx, k_out, err_word, false);
+  return check_launch("detect_outliers");
+}
+
+}  // extern "C"

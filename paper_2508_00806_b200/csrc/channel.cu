@@ -1,0 +1,257 @@
+// K3 / K3': per-channel symmetric int4 (scheme_for(QKV_MATRIX), codec.py:76-77).
+//
+// Reference semantics: group c = column c over all rows (_grouped_view with
+// PER_CHANNEL, codec.py:181-182), scale_c = f16(max_r |h[r,c]| / 8), codes
+// packed COLUMN-major, i.e. nibble index c*rows + r (codec.py:232-233).
+//
+// Two kernels:
+//   channel_absmax  -- one read of x (kept in L2 with evict_last), per-column
+//                      abs-max as f16 bit patterns, atomicMax into workspace;
+//   channel_quant   -- re-reads x (L2-resident for activation-sized tensors),
+//                      quantises a 64-column x 256-row block with 8 column
+//                      scales held in registers, transposes row-major codes
+//                      into column-major bytes with warp shuffles + a 2 KB
+//                      shared-memory stage, writes 16-byte column runs.
+//   channel_dequant -- the inverse transpose.
+// Fast path needs cols % 8 == 0 and rows % 32 == 0; anything else goes to the
+// generic kernels in group.cu.
+#include "common.cuh"
+#include "launch.h"
+
+namespace adc {
+
+constexpr int kTileCols = 64;     // 8 column units of 8
+constexpr int kSubRows = 64;      // rows per sub-tile (32 row pairs)
+constexpr int kBlockRows = 256;   // rows per block (4 sub-tiles)
+constexpr int kWordStride = 9;    // padded smem stride (words) per column
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+    channel_absmax(const void *__restrict__ x, int64_t rows, int64_t cols,
+                   uint32_t *__restrict__ colmax, uint32_t *__restrict__ err) {
+  __shared__ uint32_t red[8][32][4];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int64_t cu = static_cast<int64_t>(blockIdx.x) * 32 + tx;  // column unit
+  const bool live = cu * 8 < cols;
+  uint32_t m[4] = {0, 0, 0, 0};
+  if (live) {
+    for (int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + ty; r < rows;
+         r += static_cast<int64_t>(gridDim.y) * 8) {
+      uint4 h = Loader<DT>::template load8<true>(x, r * cols + cu * 8);
+      m[0] = __vmaxu2(m[0], h.x & 0x7fff7fffu);
+      m[1] = __vmaxu2(m[1], h.y & 0x7fff7fffu);
+      m[2] = __vmaxu2(m[2], h.z & 0x7fff7fffu);
+      m[3] = __vmaxu2(m[3], h.w & 0x7fff7fffu);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) red[ty][tx][j] = m[j];
+  __syncthreads();
+  if (ty == 0 && live) {
+    bool bad = false;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t v = red[0][tx][j];
+#pragma unroll
+      for (int t = 1; t < 8; ++t) v = __vmaxu2(v, red[t][tx][j]);
+      uint32_t lo = v & 0xffffu, hi = v >> 16;
+      bad |= lo >= 0x7c00u || hi >= 0x7c00u;
+      atomicMax(colmax + cu * 8 + 2 * j, lo);
+      atomicMax(colmax + cu * 8 + 2 * j + 1, hi);
+    }
+    if (bad) raise_err(err, ADC_ERR_NONFINITE);
+  }
+}
+
+// Byte `b` of word w.
+__device__ __forceinline__ uint32_t byte_of(uint32_t w, int b) { return (w >> (8 * b)) & 0xffu; }
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+    channel_quant(const void *__restrict__ x, int64_t rows, int64_t cols,
+                  const uint32_t *__restrict__ colmax, uint8_t *__restrict__ codes,
+                  uint16_t *__restrict__ scales) {
+  __shared__ uint32_t stage[kTileCols * kWordStride];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = lane & 7;         // column unit inside the tile
+  const int tyl = lane >> 3;       // row pair inside the warp (0..3)
+  const int rp = warp * 4 + tyl;   // row pair inside the sub-tile (0..31)
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTileCols + tx * 8;
+  const bool col_live = c0 < cols;
+
+  // Per-column quantisation constants for this thread's 8 columns.
+  float qs[8], qi[8];
+  {
+    uint32_t sb[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint32_t top = col_live ? __ldg(colmax + c0 + j) : 0u;
+      sb[j] = sym_scale_bits(top);
+      QParams q = make_qparams(static_cast<uint16_t>(sb[j]), 0);
+      qs[j] = q.s;
+      qi[j] = q.inv;
+    }
+    if (blockIdx.y == 0 && warp == 0 && tyl == 0 && col_live) {
+      uint4 v = make_uint4(sb[0] | (sb[1] << 16), sb[2] | (sb[3] << 16), sb[4] | (sb[5] << 16),
+                           sb[6] | (sb[7] << 16));
+      *reinterpret_cast<uint4 *>(scales + c0) = v;
+    }
+  }
+
+  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
+  for (int sub = 0; sub < kBlockRows / kSubRows; ++sub) {
+    const int64_t r0 = row_begin + sub * kSubRows;
+    if (r0 >= rows) break;
+    const int64_t r = r0 + 2 * rp;
+    const bool live = col_live && r < rows;  // rows % 32 == 0 => r+1 < rows too
+    uint4 ha = make_uint4(0, 0, 0, 0), hb = make_uint4(0, 0, 0, 0);
+    if (live) {
+      ha = Loader<DT>::template load8<false>(x, r * cols + c0);
+      hb = Loader<DT>::template load8<false>(x, (r + 1) * cols + c0);
+    }
+    // byte j = code(row r, col j) | code(row r+1, col j) << 4
+    uint32_t lo = 0, hi = 0;
+    {
+      uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w};
+      uint32_t wb[4] = {hb.x, hb.y, hb.z, hb.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t sh = (j & 1) * 16;
+        const float a = h2f((wa[j >> 1] >> sh) & 0xffffu);
+        const float b = h2f((wb[j >> 1] >> sh) & 0xffffu);
+        QParams q;
+        q.s = qs[j];
+        q.inv = qi[j];
+        q.o = 0.f;
+        const uint32_t byte = (static_cast<uint32_t>(sym_code(a, q)) & 0xfu) |
+                              ((static_cast<uint32_t>(sym_code(b, q)) & 0xfu) << 4);
+        if (j < 4)
+          lo |= byte << (8 * j);
+        else
+          hi |= byte << (8 * (j - 4));
+      }
+    }
+    // 4x4 byte transpose among the 4 lanes sharing tx: afterwards this lane
+    // holds, for column (tx*8 + tyl) [lo] and (tx*8 + 4 + tyl) [hi], the bytes
+    // of row pairs warp*4 + 0..3.
+    uint32_t tlo = 0, thi = 0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const uint32_t plo = __shfl_sync(0xffffffffu, lo, t * 8 + tx);
+      const uint32_t phi = __shfl_sync(0xffffffffu, hi, t * 8 + tx);
+      tlo |= byte_of(plo, tyl) << (8 * t);
+      thi |= byte_of(phi, tyl) << (8 * t);
+    }
+    __syncthreads();  // previous sub-tile's stage has been drained
+    stage[(tx * 8 + tyl) * kWordStride + warp] = tlo;
+    stage[(tx * 8 + 4 + tyl) * kWordStride + warp] = thi;
+    __syncthreads();
+    if (threadIdx.x < kTileCols * 2) {
+      const int c = threadIdx.x >> 1, h = threadIdx.x & 1;
+      const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
+      const int64_t rs = r0 + 32 * h;
+      if (cg < cols && rs < rows) {
+        const uint32_t *s = stage + c * kWordStride + 4 * h;
+        uint4 v = make_uint4(s[0], s[1], s[2], s[3]);
+        st_stream16(codes + (cg * rows + rs) / 2, v);
+      }
+    }
+  }
+}
+
+template <int OT>
+__global__ void __launch_bounds__(kThreads)
+    channel_dequant(const uint8_t *__restrict__ codes, const uint16_t *__restrict__ scales,
+                    int64_t rows, int64_t cols, void *__restrict__ y) {
+  __shared__ uint32_t stage[kTileCols * kWordStride];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int tx = lane & 7, tyl = lane >> 3;
+  const int rp = warp * 4 + tyl;
+  const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTileCols + tx * 8;
+  const bool col_live = c0 < cols;
+  float sc[8];
+  {
+    uint4 v = col_live ? __ldg(reinterpret_cast<const uint4 *>(scales + c0)) : make_uint4(0, 0, 0, 0);
+    uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int j = 0; j < 8; ++j) sc[j] = h2f((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
+  }
+  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
+  for (int sub = 0; sub < kBlockRows / kSubRows; ++sub) {
+    const int64_t r0 = row_begin + sub * kSubRows;
+    if (r0 >= rows) break;
+    __syncthreads();
+    if (threadIdx.x < kTileCols * 2) {
+      const int c = threadIdx.x >> 1, h = threadIdx.x & 1;
+      const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
+      const int64_t rs = r0 + 32 * h;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (cg < cols && rs < rows) v = ld_stream16(codes + (cg * rows + rs) / 2);
+      uint32_t *s = stage + c * kWordStride + 4 * h;
+      s[0] = v.x;
+      s[1] = v.y;
+      s[2] = v.z;
+      s[3] = v.w;
+    }
+    __syncthreads();
+    const int64_t r = r0 + 2 * rp;
+    if (!col_live || r >= rows) continue;
+    float va[8], vb[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const uint32_t word = stage[(tx * 8 + j) * kWordStride + warp];
+      const uint32_t byte = byte_of(word, tyl);
+      va[j] = nib_code(byte, 0) * sc[j];
+      vb[j] = nib_code(byte, 1) * sc[j];
+    }
+    Storer<OT>::store8(y, r * cols + c0, va);
+    Storer<OT>::store8(y, (r + 1) * cols + c0, vb);
+  }
+}
+
+#define ADC_DT_SWITCH(dt, DT, ...)                                   \
+  switch (dt) {                                                      \
+    case ADC_F32: { constexpr int DT = ADC_F32; __VA_ARGS__; break; }  \
+    case ADC_BF16: { constexpr int DT = ADC_BF16; __VA_ARGS__; break; } \
+    case ADC_F16: { constexpr int DT = ADC_F16; __VA_ARGS__; break; }  \
+    default: return -1;                                              \
+  }
+
+static inline bool al(const void *p, size_t a) { return reinterpret_cast<uintptr_t>(p) % a == 0; }
+
+bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,
+                     const void *scales) {
+  return cols % 8 == 0 && rows % 32 == 0 && al(x, 16) && al(codes, 16) && al(scales, 16);
+}
+
+int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                            const Workspace &ws, uint8_t *codes, uint16_t *scales,
+                            uint32_t *err) {
+  if (cudaMemsetAsync(ws.colmax, 0, sizeof(uint32_t) * cols, c.stream) != cudaSuccess) return -2;
+  dim3 ga(static_cast<unsigned>((cols / 8 + 31) / 32), 1);
+  int64_t want = static_cast<int64_t>(c.num_sms) * 8 / ga.x;
+  int64_t maxy = (rows + 7) / 8;
+  ga.y = static_cast<unsigned>(want < 1 ? 1 : (want > maxy ? maxy : want));
+  dim3 gq(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
+          static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
+  ADC_DT_SWITCH(dt, DT, {
+    channel_absmax<DT><<<ga, kThreads, 0, c.stream>>>(x, rows, cols, ws.colmax, err), note_launches(1);
+    channel_quant<DT><<<gq, kThreads, 0, c.stream>>>(x, rows, cols, ws.colmax, codes, scales), note_launches(1);
+  });
+  return 0;
+}
+
+int launch_channel_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                              int64_t rows, int64_t cols, void *y, int ot) {
+  dim3 g(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
+         static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
+  switch (ot) {
+    case ADC_F32: channel_dequant<ADC_F32><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
+    case ADC_BF16: channel_dequant<ADC_BF16><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
+    case ADC_F16: channel_dequant<ADC_F16><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
+    default: return -1;
+  }
+  return 0;
+}
+
+}  // namespace adc

@@ -1,0 +1,322 @@
+// Device helpers shared by the compressor kernels (sm_100a).
+//
+// Numeric contract: SURVEY.md Appendix A, restating codec.py:156-286.
+//  * every input element is cast to float16 RNE first (codec.py:158);
+//  * scales / offsets are float16 values computed as f16(f64 expression);
+//  * codes are rint-half-even of the float64 quotient, clipped to [-8, 7];
+//  * dequantisation is one rounding of code*s (+o) to float32.
+// The helpers below reproduce those float64 results with float32 arithmetic
+// where that is provably exact, and fall back to float64 per element only on
+// exact half-integer quotients of the asymmetric scheme (Appendix A.5).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <stdint.h>
+
+#include "../../include/adacc.h"
+
+namespace adc {
+
+constexpr int kThreads = 256;
+
+// ---------------------------------------------------------------------------
+// loads: 8 consecutive elements -> 8 float16 (as 4 x half2 packed in uint4)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream16(const void *p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// Keeps the line in L2 for a second pass of the same kernel sequence
+// (evict_last cache policy; the plain .L2::evict_last qualifier is only legal
+// on 256-bit loads).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint4 ld_keep16(const void *p) {
+  uint4 r;
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+      "ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], pol;\n\t}"
+      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+      : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream16(void *p, uint4 v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w));
+}
+
+__device__ __forceinline__ uint32_t f32x2_to_h2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);  // F2FP.F16.F32.PACK_AB, RNE
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+// bf16 pair (packed in one u32) -> f16 pair.  bf16 -> f32 is exact, so the
+// only rounding is the f32 -> f16 RNE one, as numpy's astype(float16) of the
+// float32 value would do.
+__device__ __forceinline__ uint32_t bf2_to_h2(uint32_t u) {
+  return f32x2_to_h2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+
+template <int DT>
+struct Loader;
+
+template <>
+struct Loader<ADC_F16> {
+  static constexpr int kBytes = 2;
+  template <bool KEEP>
+  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
+    const char *p = static_cast<const char *>(x) + i * 2;
+    return KEEP ? ld_keep16(p) : ld_stream16(p);
+  }
+  __device__ __forceinline__ static uint16_t load1(const void *x, int64_t i) {
+    return static_cast<const uint16_t *>(x)[i];
+  }
+};
+
+template <>
+struct Loader<ADC_BF16> {
+  static constexpr int kBytes = 2;
+  template <bool KEEP>
+  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
+    const char *p = static_cast<const char *>(x) + i * 2;
+    uint4 v = KEEP ? ld_keep16(p) : ld_stream16(p);
+    return make_uint4(bf2_to_h2(v.x), bf2_to_h2(v.y), bf2_to_h2(v.z), bf2_to_h2(v.w));
+  }
+  __device__ __forceinline__ static uint16_t load1(const void *x, int64_t i) {
+    uint32_t u = static_cast<const uint16_t *>(x)[i];
+    return __half_as_ushort(__float2half_rn(__uint_as_float(u << 16)));
+  }
+};
+
+template <>
+struct Loader<ADC_F32> {
+  static constexpr int kBytes = 4;
+  template <bool KEEP>
+  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
+    const char *p = static_cast<const char *>(x) + i * 4;
+    uint4 a = KEEP ? ld_keep16(p) : ld_stream16(p);
+    uint4 b = KEEP ? ld_keep16(p + 16) : ld_stream16(p + 16);
+    return make_uint4(f32x2_to_h2(__uint_as_float(a.x), __uint_as_float(a.y)),
+                      f32x2_to_h2(__uint_as_float(a.z), __uint_as_float(a.w)),
+                      f32x2_to_h2(__uint_as_float(b.x), __uint_as_float(b.y)),
+                      f32x2_to_h2(__uint_as_float(b.z), __uint_as_float(b.w)));
+  }
+  __device__ __forceinline__ static uint16_t load1(const void *x, int64_t i) {
+    return __half_as_ushort(__float2half_rn(static_cast<const float *>(x)[i]));
+  }
+};
+
+// ---------------------------------------------------------------------------
+// float16 bit tricks
+// ---------------------------------------------------------------------------
+// |h| as an integer orders like the magnitude for finite f16; >= 0x7c00 means
+// inf/NaN, so one integer max gives both the group abs-max and the finiteness
+// check of codec.py:167-170.
+__device__ __forceinline__ uint32_t absmax8(uint4 h) {
+  uint32_t m = __vmaxu2(h.x & 0x7fff7fffu, h.y & 0x7fff7fffu);
+  m = __vmaxu2(m, h.z & 0x7fff7fffu);
+  m = __vmaxu2(m, h.w & 0x7fff7fffu);
+  return m;  // two u16 lanes
+}
+
+// Monotone unsigned key of an f16 bit pattern (-0 sorts just below +0).
+__device__ __forceinline__ uint32_t f16_key(uint32_t b) {
+  return (b & 0x8000u) ? (~b & 0xffffu) : (b | 0x8000u);
+}
+__device__ __forceinline__ uint32_t f16_unkey(uint32_t k) {
+  return (k & 0x8000u) ? (k & 0x7fffu) : (~k & 0xffffu);
+}
+// Same on both lanes of a packed pair.
+__device__ __forceinline__ uint32_t f16_key2(uint32_t b) {
+  uint32_t neg = ((b >> 15) & 0x00010001u) * 0xffffu;  // lane mask of negative lanes
+  return (b ^ (neg | 0x80008000u));
+}
+
+__device__ __forceinline__ float h2f(uint32_t bits16) {
+  return __half2float(__ushort_as_half(static_cast<uint16_t>(bits16)));
+}
+
+// codec.py:192-196: f16(raw) with a 2^-24 floor when a non-zero raw underflows.
+__device__ __forceinline__ uint16_t store_scale_f32(float raw) {
+  uint16_t s = __half_as_ushort(__float2half_rn(raw));
+  if ((s & 0x7fffu) == 0 && raw > 0.f) s = 0x0001u;
+  return s;
+}
+__device__ __forceinline__ uint16_t store_scale_f64(double raw) {
+  uint16_t s = __half_as_ushort(__double2half(raw));  // cvt.rn.f16.f64, one rounding
+  if ((s & 0x7fffu) == 0 && raw > 0.0) s = 0x0001u;
+  return s;
+}
+
+// Symmetric scale from the group abs-max bits: top/8 is exact in f32, so the
+// single f32->f16 rounding equals the reference's f64->f16 one.
+__device__ __forceinline__ uint16_t sym_scale_bits(uint32_t top_bits) {
+  return store_scale_f32(h2f(top_bits) * 0.125f);
+}
+
+// Asymmetric offset / scale from the group hi / lo (f16 bits), in float64
+// exactly as codec.py:219-222 (hi+lo and hi-lo are exact in f64).
+__device__ __forceinline__ void asym_params(uint32_t hi_bits, uint32_t lo_bits, uint16_t &off,
+                                            uint16_t &scl) {
+  double hi = static_cast<double>(h2f(hi_bits));
+  double lo = static_cast<double>(h2f(lo_bits));
+  off = __half_as_ushort(__double2half((hi + lo) * 0.5));
+  scl = store_scale_f64((hi - lo) * 0.0625);
+}
+
+// Per-group quantisation constants.
+struct QParams {
+  float s;    // divisor: the stored scale, or 1 when it is zero (codec.py:229-230)
+  float inv;  // RN(1/s)
+  float o;    // offset (0 for symmetric)
+};
+
+__device__ __forceinline__ QParams make_qparams(uint16_t s_bits, uint16_t o_bits) {
+  QParams q;
+  float s = h2f(s_bits);
+  q.s = (s == 0.f) ? 1.f : s;
+  q.inv = __frcp_rn(q.s);
+  q.o = h2f(o_bits);
+  return q;
+}
+
+constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds to int, RNE
+
+// Symmetric code of one element as an int in [-8, 7].
+// r1 is the correctly rounded f32 quotient h/s (Markstein: r0 = h*inv,
+// residual exact by FMA, one correction).  Symmetric quotients are either
+// exact half-integers (then r1 is exact and the RNE add ties to even) or at
+// least 2^-12 away from one (Appendix A.5), so this equals rint(f64(h)/s).
+__device__ __forceinline__ int sym_code(float h, const QParams &q) {
+  float r0 = h * q.inv;
+  float rem = fmaf(-r0, q.s, h);
+  float r1 = fmaf(rem, q.inv, r0);
+  r1 = fminf(fmaxf(r1, -8.f), 7.f);
+  return __float_as_int(r1 + kMagic) - 0x4B400000;
+}
+
+// Asymmetric code: d = f32(h - o) can round, but RN is monotone and every
+// decision boundary (k+1/2)*s is an f32 value, so a non-tie quotient lands on
+// the correct side; an exact half-integer quotient is re-done in float64
+// (codec.py:223-231 semantics), which is the rare slow path.
+static __device__ __noinline__ int asym_code_f64(float h, const QParams &q) {
+  double d = static_cast<double>(h) - static_cast<double>(q.o);
+  double r = rint(d / static_cast<double>(q.s));
+  r = fmin(fmax(r, -8.0), 7.0);
+  return static_cast<int>(r);
+}
+
+__device__ __forceinline__ int asym_code(float h, const QParams &q) {
+  float d = h - q.o;
+  float r0 = d * q.inv;
+  float rem = fmaf(-r0, q.s, d);
+  float r1 = fmaf(rem, q.inv, r0);
+  float c = (r1 + kMagic) - kMagic;
+  if (fabsf(r1 - c) == 0.5f) return asym_code_f64(h, q);
+  c = fminf(fmaxf(c, -8.f), 7.f);
+  return static_cast<int>(c);
+}
+
+template <bool ASYM>
+__device__ __forceinline__ int quant_code(float h, const QParams &q) {
+  if (ASYM) return asym_code(h, q);
+  return sym_code(h, q);
+}
+
+// Quantise 8 f16 values (packed) and pack 8 nibbles into one u32, element 0
+// in the lowest nibble (codec.py:199-203).
+template <bool ASYM>
+__device__ __forceinline__ uint32_t quant_pack8(uint4 h, const QParams &q) {
+  uint32_t w[4] = {h.x, h.y, h.z, h.w};
+  uint32_t out = 0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int c0 = quant_code<ASYM>(h2f(w[j] & 0xffffu), q);
+    int c1 = quant_code<ASYM>(h2f(w[j] >> 16), q);
+    out |= (static_cast<uint32_t>(c0) & 0xfu) << (8 * j);
+    out |= (static_cast<uint32_t>(c1) & 0xfu) << (8 * j + 4);
+  }
+  return out;
+}
+
+// Signed code of nibble j of a packed word.
+__device__ __forceinline__ float nib_code(uint32_t w, int j) {
+  uint32_t n = (w >> (4 * j)) & 0xfu;
+  // (n ^ 8) - 8 sign-extends the 4-bit two's complement value.
+  return __int_as_float(0x4B400000 | (n ^ 8u)) - (kMagic + 8.f);
+}
+
+// Dequantised value: code*s is exact in f32; code*s + o is one FMA rounding,
+// identical to the reference's float64 sum rounded to float32 (Appendix A.8).
+template <bool ASYM>
+__device__ __forceinline__ float deq(float code, float s, float o) {
+  return ASYM ? fmaf(code, s, o) : code * s;
+}
+
+// ---------------------------------------------------------------------------
+// output stores
+// ---------------------------------------------------------------------------
+template <int OT>
+struct Storer;
+
+template <>
+struct Storer<ADC_F32> {
+  static constexpr int kBytes = 4;
+  __device__ __forceinline__ static void store8(void *y, int64_t i, const float *v) {
+    char *p = static_cast<char *>(y) + i * 4;
+    st_stream16(p, make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                              __float_as_uint(v[2]), __float_as_uint(v[3])));
+    st_stream16(p + 16, make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]),
+                                   __float_as_uint(v[6]), __float_as_uint(v[7])));
+  }
+  __device__ __forceinline__ static void store1(void *y, int64_t i, float v) {
+    static_cast<float *>(y)[i] = v;
+  }
+};
+
+__device__ __forceinline__ uint32_t pack_bf2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+
+template <>
+struct Storer<ADC_BF16> {
+  static constexpr int kBytes = 2;
+  __device__ __forceinline__ static void store8(void *y, int64_t i, const float *v) {
+    st_stream16(static_cast<char *>(y) + i * 2,
+                make_uint4(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]), pack_bf2(v[4], v[5]),
+                           pack_bf2(v[6], v[7])));
+  }
+  __device__ __forceinline__ static void store1(void *y, int64_t i, float v) {
+    static_cast<__nv_bfloat16 *>(y)[i] = __float2bfloat16_rn(v);
+  }
+};
+
+template <>
+struct Storer<ADC_F16> {
+  static constexpr int kBytes = 2;
+  __device__ __forceinline__ static void store8(void *y, int64_t i, const float *v) {
+    st_stream16(static_cast<char *>(y) + i * 2,
+                make_uint4(f32x2_to_h2(v[0], v[1]), f32x2_to_h2(v[2], v[3]),
+                           f32x2_to_h2(v[4], v[5]), f32x2_to_h2(v[6], v[7])));
+  }
+  __device__ __forceinline__ static void store1(void *y, int64_t i, float v) {
+    static_cast<__half *>(y)[i] = __float2half_rn(v);
+  }
+};
+
+__device__ __forceinline__ void raise_err(uint32_t *err, uint32_t bit) {
+  if (err) atomicOr(err, bit);
+}
+
+}  // namespace adc

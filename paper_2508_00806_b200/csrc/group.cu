@@ -1,0 +1,439 @@
+// K1/K2 (symmetric / asymmetric group int4) compress + decompress, the
+// outlier-zeroing variant used by K4, and the generic any-shape fallbacks.
+//
+// Reference: _quantize (codec.py:216-242), quantize_symmetric (:245-252),
+// quantize_asymmetric (:255-258), dequantize (:261-286).
+//
+// Fast path layout: one thread owns 8 consecutive elements ("unit"): one
+// 128-bit load (bf16/f16; two for f32), one 32-bit store of 8 packed nibbles.
+// A group of g = 8*L elements is owned by L adjacent lanes of a warp and
+// reduced with L-wide xor shuffles; every lane derives the group's scale
+// itself (no broadcast), lane 0 of the group stores it.
+#include "common.cuh"
+#include "launch.h"
+
+namespace adc {
+
+__device__ __forceinline__ uint32_t fastdiv(uint32_t n, const FastDiv &f) {
+  return static_cast<uint32_t>((static_cast<uint64_t>(n) * f.m) >> f.p);
+}
+
+template <int L>
+__device__ __forceinline__ uint32_t warp_max_u2(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+template <int L>
+__device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
+#pragma unroll
+  for (int o = 1; o < L; o <<= 1) v = __vminu2(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// Zero the flagged channels of one unit (codec.py:328-329) and copy their
+// original f16 values into the (k, rows) side buffer (codec.py:340).  The
+// flag test is inline; the rare hit path is out of line to keep registers.
+__device__ __noinline__ void zero_outlier_hit(uint4 &h, uint2 f, uint32_t r, uint32_t c,
+                                              const int32_t *__restrict__ rank,
+                                              uint16_t *__restrict__ outl_val, int64_t rows,
+                                              int64_t k_cap) {
+  uint32_t w[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    uint32_t fb = ((j < 4 ? f.x : f.y) >> (8 * (j & 3))) & 0xffu;
+    if (fb) {
+      uint32_t bits = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+      int32_t rk = __ldg(rank + c + j);
+      if (rk >= 0 && rk < k_cap) outl_val[static_cast<int64_t>(rk) * rows + r] = bits;
+      w[j >> 1] &= (j & 1) ? 0x0000ffffu : 0xffff0000u;
+    }
+  }
+  h = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+__device__ __forceinline__ void zero_outlier_lanes(uint4 &h, int64_t e, const FastDiv &dc,
+                                                   const uint8_t *__restrict__ zflag,
+                                                   const int32_t *__restrict__ rank,
+                                                   uint16_t *__restrict__ outl_val, int64_t rows,
+                                                   int64_t k_cap) {
+  uint32_t r = fastdiv(static_cast<uint32_t>(e), dc);
+  uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
+  uint2 f = __ldg(reinterpret_cast<const uint2 *>(zflag + c));
+  if ((f.x | f.y) != 0) zero_outlier_hit(h, f, r, c, rank, outl_val, rows, k_cap);
+}
+
+template <int DT, bool ASYM, int L, bool ZERO, int U>
+__global__ void __launch_bounds__(kThreads)
+    group_quant_fast(const void *__restrict__ x, int64_t n_units, int64_t n_units_pad, FastDiv dc,
+                     int64_t rows, const uint8_t *__restrict__ zflag,
+                     const int32_t *__restrict__ rank, uint16_t *__restrict__ outl_val,
+                     int64_t k_cap, uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
+                     uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units_pad;
+       base += step) {
+    uint4 h[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      int64_t u = base + k * kThreads + threadIdx.x;
+      h[k] = (u < n_units) ? Loader<DT>::template load8<false>(x, u * 8) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t u = base + k * kThreads + threadIdx.x;
+      const bool act = u < n_units;
+      if (ZERO && act) zero_outlier_lanes(h[k], u * 8, dc, zflag, rank, outl_val, rows, k_cap);
+      uint16_t s_bits, o_bits = 0;
+      bool bad;
+      if (ASYM) {
+        uint32_t kx0 = f16_key2(h[k].x), kx1 = f16_key2(h[k].y);
+        uint32_t kx2 = f16_key2(h[k].z), kx3 = f16_key2(h[k].w);
+        uint32_t kmax = act ? __vmaxu2(__vmaxu2(kx0, kx1), __vmaxu2(kx2, kx3)) : 0u;
+        uint32_t kmin = act ? __vminu2(__vminu2(kx0, kx1), __vminu2(kx2, kx3)) : 0xffffffffu;
+        kmax = warp_max_u2<L>(kmax);
+        kmin = warp_min_u2<L>(kmin);
+        uint32_t hi = f16_unkey(max(kmax & 0xffffu, kmax >> 16));
+        uint32_t lo = f16_unkey(min(kmin & 0xffffu, kmin >> 16));
+        bad = ((hi & 0x7fffu) >= 0x7c00u) || ((lo & 0x7fffu) >= 0x7c00u);
+        asym_params(hi, lo, o_bits, s_bits);
+      } else {
+        uint32_t m = act ? absmax8(h[k]) : 0u;
+        m = warp_max_u2<L>(m);
+        uint32_t top = max(m & 0xffffu, m >> 16);
+        bad = top >= 0x7c00u;
+        s_bits = sym_scale_bits(top);
+      }
+      const int64_t grp = u / L;
+      if ((threadIdx.x & (L - 1)) == 0 && u < n_units_pad) {
+        if (bad) raise_err(err, ADC_ERR_NONFINITE);
+        scales[grp] = s_bits;
+        if (ASYM) offsets[grp] = o_bits;
+      }
+      if (act) {
+        QParams q = make_qparams(s_bits, o_bits);
+        codes[u] = quant_pack8<ASYM>(h[k], q);
+      }
+    }
+  }
+}
+
+template <int OT, bool ASYM, int L, int U>
+__global__ void __launch_bounds__(kThreads)
+    group_dequant_fast(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
+                       const uint16_t *__restrict__ offsets, int64_t n_units, void *__restrict__ y) {
+  const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
+  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units;
+       base += step) {
+    uint32_t w[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      int64_t u = base + k * kThreads + threadIdx.x;
+      w[k] = (u < n_units) ? __ldcs(codes + u) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      int64_t u = base + k * kThreads + threadIdx.x;
+      if (u >= n_units) continue;
+      const int64_t grp = u / L;
+      float s = h2f(__ldg(scales + grp));
+      float o = ASYM ? h2f(__ldg(offsets + grp)) : 0.f;
+      float v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = deq<ASYM>(nib_code(w[k], j), s, o);
+      Storer<OT>::store8(y, u * 8, v);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic fallbacks: any group size (incl. PER_CHANNEL), any shape/alignment
+// ---------------------------------------------------------------------------
+template <int DT, bool ASYM>
+__global__ void __launch_bounds__(kThreads)
+    group_stats_generic(const void *__restrict__ x, int64_t n, int64_t g, int64_t n_groups,
+                        bool pc, int64_t rows, int64_t cols, const uint8_t *__restrict__ zflag,
+                        uint16_t *__restrict__ scales, uint16_t *__restrict__ offsets,
+                        uint32_t *__restrict__ err) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
+  for (int64_t j = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + threadIdx.x / 32;
+       j < n_groups; j += warps) {
+    const int64_t count = pc ? rows : min(g, n - j * g);
+    uint32_t amax = 0, kmax = 0, kmin = 0xffffu;
+    bool bad = false;
+    for (int64_t i = lane; i < count; i += 32) {
+      const int64_t e = pc ? i * cols + j : j * g + i;
+      uint32_t b = Loader<DT>::load1(x, e);
+      bad |= (b & 0x7fffu) >= 0x7c00u;
+      if (zflag && zflag[e % cols]) b = 0;
+      amax = max(amax, b & 0x7fffu);
+      kmax = max(kmax, f16_key(b));
+      kmin = min(kmin, f16_key(b));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      kmax = max(kmax, __shfl_xor_sync(0xffffffffu, kmax, o));
+      kmin = min(kmin, __shfl_xor_sync(0xffffffffu, kmin, o));
+    }
+    bad = __any_sync(0xffffffffu, bad);
+    if (lane == 0) {
+      if (bad) raise_err(err, ADC_ERR_NONFINITE);
+      if (ASYM) {
+        uint16_t o, s;
+        asym_params(f16_unkey(kmax), f16_unkey(kmin), o, s);
+        scales[j] = s;
+        offsets[j] = o;
+      } else {
+        scales[j] = sym_scale_bits(amax);
+      }
+    }
+  }
+}
+
+template <int DT, bool ASYM>
+__global__ void __launch_bounds__(kThreads)
+    group_quant_generic(const void *__restrict__ x, int64_t n, int64_t g, bool pc, int64_t rows,
+                        int64_t cols, const uint8_t *__restrict__ zflag,
+                        const uint16_t *__restrict__ scales, const uint16_t *__restrict__ offsets,
+                        uint8_t *__restrict__ codes) {
+  const int64_t nbytes = (n + 1) / 2;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
+       b += static_cast<int64_t>(gridDim.x) * kThreads) {
+    uint32_t byte = 0;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int64_t p = 2 * b + half;  // position in the code stream
+      if (p >= n) break;
+      int64_t r, c, grp;
+      if (pc) {
+        c = p / rows;
+        r = p - c * rows;
+        grp = c;
+      } else {
+        r = p / cols;
+        c = p - r * cols;
+        grp = p / g;
+      }
+      uint32_t hb = Loader<DT>::load1(x, r * cols + c);
+      if (zflag && zflag[c]) hb = 0;
+      QParams q = make_qparams(scales[grp], ASYM ? offsets[grp] : 0);
+      int code = quant_code<ASYM>(h2f(hb), q);
+      byte |= (static_cast<uint32_t>(code) & 0xfu) << (4 * half);
+    }
+    codes[b] = static_cast<uint8_t>(byte);
+  }
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads)
+    outlier_gather_generic(const void *__restrict__ x, const uint32_t *__restrict__ idx,
+                           const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows,
+                           int64_t cols, uint16_t *__restrict__ outl_val) {
+  const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < k * rows;
+       t += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t i = t / rows, r = t - i * rows;
+    outl_val[t] = Loader<DT>::load1(x, r * cols + idx[i]);
+  }
+}
+
+template <int OT, bool ASYM>
+__global__ void __launch_bounds__(kThreads)
+    group_dequant_generic(const uint8_t *__restrict__ codes, const uint16_t *__restrict__ scales,
+                          const uint16_t *__restrict__ offsets, int64_t n, int64_t g, bool pc,
+                          int64_t rows, int64_t cols, void *__restrict__ y) {
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t r = e / cols, c = e - r * cols;
+    const int64_t p = pc ? c * rows + r : e;
+    const int64_t grp = pc ? c : p / g;
+    const uint32_t nib = (codes[p >> 1] >> ((p & 1) * 4)) & 0xfu;
+    const float code = __int_as_float(0x4B400000 | (nib ^ 8u)) - (kMagic + 8.f);
+    const float s = h2f(scales[grp]);
+    const float o = ASYM ? h2f(offsets[grp]) : 0.f;
+    Storer<OT>::store1(y, e, deq<ASYM>(code, s, o));
+  }
+}
+
+template <int OT>
+__global__ void __launch_bounds__(kThreads)
+    outlier_scatter(const uint32_t *__restrict__ idx, const uint16_t *__restrict__ val,
+                    const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                    void *__restrict__ y) {
+  const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
+  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < k * rows;
+       t += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const int64_t i = t / rows, r = t - i * rows;
+    Storer<OT>::store1(y, r * cols + idx[i], h2f(val[t]));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------
+static inline int grid_for(const Ctx &c, int64_t work_items, int per_block) {
+  int64_t need = (work_items + per_block - 1) / per_block;
+  int64_t cap = static_cast<int64_t>(c.num_sms) * 8;
+  if (need < 1) need = 1;
+  return static_cast<int>(need < cap ? need : cap);
+}
+
+static inline bool aligned(const void *p, size_t a) {
+  return (reinterpret_cast<uintptr_t>(p) % a) == 0;
+}
+
+static inline int lanes_for_group(int64_t g) {
+  switch (g) {
+    case 8: return 1;
+    case 16: return 2;
+    case 32: return 4;
+    case 64: return 8;
+    case 128: return 16;
+    case 256: return 32;
+    default: return 0;
+  }
+}
+
+#define ADC_DT_SWITCH(dt, DT, ...)                                   \
+  switch (dt) {                                                      \
+    case ADC_F32: { constexpr int DT = ADC_F32; __VA_ARGS__; break; }  \
+    case ADC_BF16: { constexpr int DT = ADC_BF16; __VA_ARGS__; break; } \
+    case ADC_F16: { constexpr int DT = ADC_F16; __VA_ARGS__; break; }  \
+    default: return -1;                                              \
+  }
+
+#define ADC_L_SWITCH(l, L, ...)                         \
+  switch (l) {                                          \
+    case 1: { constexpr int L = 1; __VA_ARGS__; break; }  \
+    case 2: { constexpr int L = 2; __VA_ARGS__; break; }  \
+    case 4: { constexpr int L = 4; __VA_ARGS__; break; }  \
+    case 8: { constexpr int L = 8; __VA_ARGS__; break; }  \
+    case 16: { constexpr int L = 16; __VA_ARGS__; break; } \
+    case 32: { constexpr int L = 32; __VA_ARGS__; break; } \
+    default: return -1;                                 \
+  }
+
+constexpr int kUnroll = 2;
+
+int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                          int64_t g, bool asym, const uint8_t *zero_flag, const int32_t *rank,
+                          const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
+                          int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
+                          uint32_t *err) {
+  const int64_t n = rows * cols;
+  const bool pc = (g == 0);
+  const int L = pc ? 0 : lanes_for_group(g);
+  const bool zero = zero_flag != nullptr;
+  const bool fast = L > 0 && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) &&
+                    (!zero || (cols % 8 == 0 && n < (1ll << 31)));
+  if (fast) {
+    const int64_t n_units = n / 8;
+    const int64_t n_groups = (n_units + L - 1) / L;
+    const int64_t n_units_pad = n_groups * L;
+    const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
+    const int grid = grid_for(c, n_units_pad, kThreads * kUnroll);
+    uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
+    ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
+      if (asym) {
+        group_quant_fast<DT, true, LL, false, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
+            offsets, err), note_launches(1);
+      } else if (zero) {
+        group_quant_fast<DT, false, LL, true, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, zero_flag, rank, outl_val, k_cap, codes32, scales,
+            nullptr, err), note_launches(1);
+      } else {
+        group_quant_fast<DT, false, LL, false, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
+            nullptr, err), note_launches(1);
+      }
+    }));
+    return 0;
+  }
+  // generic: per-group stats, then per-byte quantisation
+  const int64_t n_groups = pc ? cols : (n + g - 1) / g;
+  const int gs = grid_for(c, n_groups, kThreads / 32);
+  const int gq = grid_for(c, (n + 1) / 2, kThreads);
+  ADC_DT_SWITCH(dt, DT, {
+    if (asym) {
+      group_stats_generic<DT, true><<<gs, kThreads, 0, c.stream>>>(
+          x, n, g, n_groups, pc, rows, cols, zero_flag, scales, offsets, err), note_launches(1);
+      group_quant_generic<DT, true><<<gq, kThreads, 0, c.stream>>>(x, n, g, pc, rows, cols,
+                                                                    zero_flag, scales, offsets,
+                                                                    codes), note_launches(1);
+    } else {
+      group_stats_generic<DT, false><<<gs, kThreads, 0, c.stream>>>(
+          x, n, g, n_groups, pc, rows, cols, zero_flag, scales, nullptr, err), note_launches(1);
+      group_quant_generic<DT, false><<<gq, kThreads, 0, c.stream>>>(x, n, g, pc, rows, cols,
+                                                                     zero_flag, scales, nullptr,
+                                                                     codes), note_launches(1);
+    }
+  });
+  if (zero_flag) return launch_outlier_gather(c, x, dt, idx, k_dev, k_cap, rows, cols, outl_val);
+  return 0;
+}
+
+int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
+                          const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                          uint16_t *outl_val) {
+  if (k_cap <= 0) return 0;
+  const int grid = grid_for(c, k_cap * rows, kThreads);
+  ADC_DT_SWITCH(dt, DT, outlier_gather_generic<DT><<<grid, kThreads, 0, c.stream>>>(
+                            x, idx, k_dev, k_cap, rows, cols, outl_val), note_launches(1));
+  return 0;
+}
+
+#define ADC_OT_SWITCH(ot, OT, ...)                                   \
+  switch (ot) {                                                      \
+    case ADC_F32: { constexpr int OT = ADC_F32; __VA_ARGS__; break; }  \
+    case ADC_BF16: { constexpr int OT = ADC_BF16; __VA_ARGS__; break; } \
+    case ADC_F16: { constexpr int OT = ADC_F16; __VA_ARGS__; break; }  \
+    default: return -1;                                              \
+  }
+
+int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                            const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
+                            bool asym, void *y, int ot) {
+  const int64_t n = rows * cols;
+  const bool pc = (g == 0);
+  const int L = pc ? 0 : lanes_for_group(g);
+  const bool fast = L > 0 && n % 8 == 0 && aligned(y, 16) && aligned(codes, 4);
+  if (fast) {
+    const int64_t n_units = n / 8;
+    const int grid = grid_for(c, n_units, kThreads * kUnroll);
+    const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
+    ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
+      if (asym)
+        group_dequant_fast<OT, true, LL, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            codes32, scales, offsets, n_units, y), note_launches(1);
+      else
+        group_dequant_fast<OT, false, LL, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            codes32, scales, nullptr, n_units, y), note_launches(1);
+    }));
+    return 0;
+  }
+  const int grid = grid_for(c, n, kThreads);
+  ADC_OT_SWITCH(ot, OT, {
+    if (asym)
+      group_dequant_generic<OT, true><<<grid, kThreads, 0, c.stream>>>(codes, scales, offsets, n,
+                                                                       g, pc, rows, cols, y), note_launches(1);
+    else
+      group_dequant_generic<OT, false><<<grid, kThreads, 0, c.stream>>>(codes, scales, nullptr,
+                                                                        n, g, pc, rows, cols, y), note_launches(1);
+  });
+  return 0;
+}
+
+int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
+                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                           void *y, int ot) {
+  if (k_cap <= 0) return 0;
+  const int grid = grid_for(c, k_cap * rows, kThreads);
+  ADC_OT_SWITCH(ot, OT, outlier_scatter<OT><<<grid, kThreads, 0, c.stream>>>(
+                            idx, val, k_dev, k_cap, rows, cols, y), note_launches(1));
+  return 0;
+}
+
+}  // namespace adc

@@ -1,0 +1,87 @@
+// Host-side launchers shared between the kernel translation units and the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace adc {
+
+// 32-bit division by a runtime constant: q = (n * m) >> p, exact for n < 2^31.
+struct FastDiv {
+  uint64_t m;
+  uint32_t p;
+  uint32_t d;
+};
+
+inline FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f;
+  f.d = d;
+  uint32_t l = 0;
+  while ((1ull << l) < d) ++l;
+  f.p = 31 + l;
+  f.m = ((1ull << f.p) + d - 1) / d;  // ceil(2^p / d)
+  return f;
+}
+
+// Count of kernels this library has launched (adc_kernel_launches()).
+void note_launches(int n);
+
+struct Ctx {
+  cudaStream_t stream;
+  int num_sms;
+};
+
+// Workspace carving (offsets in bytes, 256-aligned).
+struct Workspace {
+  double *colsum;        // cols       (outlier)
+  uint32_t *colmax;      // cols       (per-channel abs-max bits)
+  uint8_t *flag;         // cols       (outlier flags, padded to 8)
+  int32_t *rank;         // cols       (outlier rank of a flagged column, else -1)
+  int64_t *leaf;         // leaf table for the pairwise tree (start<<20 | len)
+  double *leafsum;       // per-leaf partial sums
+  uint32_t *misc;        // [0] inexact-sum flag, [1] leaf count
+  size_t bytes;
+};
+
+size_t workspace_layout(int64_t cols, Workspace *ws, void *base);
+
+// group kernels (group.cu)
+int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                          int64_t g, bool asym, const uint8_t *zero_flag, const int32_t *rank,
+                          const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
+                          int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
+                          uint32_t *err);
+int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                            const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
+                            bool asym, void *y, int ot);
+int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
+                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                           void *y, int ot);
+
+int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
+                          const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                          uint16_t *outl_val);
+
+// per-channel kernels (channel.cu)
+bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,
+                     const void *scales);
+int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                            const Workspace &ws, uint8_t *codes, uint16_t *scales,
+                            uint32_t *err);
+int launch_channel_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                              int64_t rows, int64_t cols, void *y, int ot);
+
+// outlier detection (outlier.cu)
+int launch_colsum(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                  const Workspace &ws, uint32_t *err);
+int launch_outlier_stats(const Ctx &c, int64_t rows, int64_t cols, double thr, int64_t k_cap,
+                         const Workspace &ws, uint32_t *idx, int32_t *k_out, uint32_t *err,
+                         bool too_many_check);
+int launch_copy_sums(const Ctx &c, const Workspace &ws, double *out, int64_t cols);
+
+// masks (mask.cu)
+int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bits,
+                     uint32_t *err);
+int launch_mask_unpack(const Ctx &c, const uint8_t *bits, int64_t n, uint8_t *out);
+
+}  // namespace adc

@@ -1,0 +1,167 @@
+// K5: dropout-mask bit packing (scheme_for(DROPOUT_MASK), codec.py:80-81).
+//
+// Reference: pack_bitmask (codec.py:344-369) -- bytes must be 0/1
+// (NonBinaryMaskError otherwise), bit (i mod 8) of byte i/8 = m[i]
+// (np.packbits bitorder="little"), zero padding; unpack_bitmask (:372-378).
+// One thread packs 64 elements into one 64-bit word.
+#include "common.cuh"
+#include "launch.h"
+
+namespace adc {
+
+// 4 bytes in {0,1} (u32) -> 4 bits; multiplier places byte j's bit 0 at bit 24+j
+__device__ __forceinline__ uint32_t gather4(uint32_t w) { return ((w * 0x01020408u) >> 24) & 0xfu; }
+// 4 bits -> 4 bytes in {0,1}
+__device__ __forceinline__ uint32_t spread4(uint32_t n) { return (n * 0x00204081u) & 0x01010101u; }
+
+template <int DT>
+struct MaskIn;
+
+template <>
+struct MaskIn<ADC_U8> {
+  // 8 elements -> 8 bits; bad if any byte not in {0,1}
+  __device__ __forceinline__ static uint32_t bits8(const void *m, int64_t i, bool &bad) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(static_cast<const uint8_t *>(m) + i);
+    bad |= ((v.x | v.y) & 0xfefefefeu) != 0;
+    return gather4(v.x) | (gather4(v.y) << 4);
+  }
+  __device__ __forceinline__ static uint32_t bit1(const void *m, int64_t i, bool &bad) {
+    const uint32_t b = static_cast<const uint8_t *>(m)[i];
+    bad |= b > 1;
+    return b & 1u;
+  }
+};
+
+template <typename T>
+__device__ __forceinline__ uint32_t fbit(T v, bool &bad) {
+  const float f = static_cast<float>(v);
+  bad |= !(f == 0.f || f == 1.f);
+  return f == 1.f;
+}
+
+template <>
+struct MaskIn<ADC_F32> {
+  __device__ __forceinline__ static uint32_t bits8(const void *m, int64_t i, bool &bad) {
+    const float4 *p = reinterpret_cast<const float4 *>(static_cast<const float *>(m) + i);
+    const float4 a = p[0], b = p[1];
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r |= fbit(v[j], bad) << j;
+    return r;
+  }
+  __device__ __forceinline__ static uint32_t bit1(const void *m, int64_t i, bool &bad) {
+    return fbit(static_cast<const float *>(m)[i], bad);
+  }
+};
+
+template <>
+struct MaskIn<ADC_BF16> {
+  __device__ __forceinline__ static uint32_t bits8(const void *m, int64_t i, bool &bad) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(m) + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float f = __uint_as_float(((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu) << 16);
+      r |= fbit(f, bad) << j;
+    }
+    return r;
+  }
+  __device__ __forceinline__ static uint32_t bit1(const void *m, int64_t i, bool &bad) {
+    const uint32_t u = static_cast<const uint16_t *>(m)[i];
+    return fbit(__uint_as_float(u << 16), bad);
+  }
+};
+
+template <>
+struct MaskIn<ADC_F16> {
+  __device__ __forceinline__ static uint32_t bits8(const void *m, int64_t i, bool &bad) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(static_cast<const uint16_t *>(m) + i);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+    uint32_t r = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r |= fbit(h2f((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu), bad) << j;
+    return r;
+  }
+  __device__ __forceinline__ static uint32_t bit1(const void *m, int64_t i, bool &bad) {
+    return fbit(h2f(static_cast<const uint16_t *>(m)[i]), bad);
+  }
+};
+
+// FAST: n % 8 == 0 and vector-aligned input; else byte-by-byte.
+template <int DT, bool FAST>
+__global__ void __launch_bounds__(kThreads)
+    mask_pack(const void *__restrict__ m, int64_t n, uint8_t *__restrict__ bits,
+              uint32_t *__restrict__ err) {
+  const int64_t nbytes = (n + 7) / 8;
+  bool bad = false;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
+       b += static_cast<int64_t>(gridDim.x) * kThreads) {
+    uint32_t v = 0;
+    if (FAST) {
+      v = MaskIn<DT>::bits8(m, b * 8, bad);
+    } else {
+      for (int j = 0; j < 8 && b * 8 + j < n; ++j) v |= MaskIn<DT>::bit1(m, b * 8 + j, bad) << j;
+    }
+    bits[b] = static_cast<uint8_t>(v);
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_err(err, ADC_ERR_NONBINARY);
+}
+
+// One thread expands one packed byte into 8 output bytes (a u64 store).
+template <bool FAST>
+__global__ void __launch_bounds__(kThreads)
+    mask_unpack(const uint8_t *__restrict__ bits, int64_t n, uint8_t *__restrict__ out) {
+  const int64_t nbytes = (n + 7) / 8;
+  for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
+       b += static_cast<int64_t>(gridDim.x) * kThreads) {
+    const uint32_t v = bits[b];
+    if (FAST) {
+      *reinterpret_cast<uint2 *>(out + b * 8) = make_uint2(spread4(v & 0xfu), spread4(v >> 4));
+    } else {
+      for (int j = 0; j < 8 && b * 8 + j < n; ++j) out[b * 8 + j] = (v >> j) & 1u;
+    }
+  }
+}
+
+static inline int grid_of(const Ctx &c, int64_t items) {
+  int64_t need = (items + kThreads - 1) / kThreads;
+  int64_t cap = static_cast<int64_t>(c.num_sms) * 16;
+  return static_cast<int>(need < 1 ? 1 : (need < cap ? need : cap));
+}
+
+int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bits,
+                     uint32_t *err) {
+  const int elt = dt == ADC_F32 ? 4 : (dt == ADC_U8 ? 1 : 2);
+  const bool fast = n % 8 == 0 && reinterpret_cast<uintptr_t>(m) % (8 * elt < 16 ? 8 * elt : 16) == 0;
+  const int grid = grid_of(c, (n + 7) / 8);
+#define ADC_MASK_CASE(DT)                                                                    \
+  case DT:                                                                                   \
+    if (fast)                                                                                \
+      mask_pack<DT, true><<<grid, kThreads, 0, c.stream>>>(m, n, bits, err), note_launches(1);                 \
+    else                                                                                     \
+      mask_pack<DT, false><<<grid, kThreads, 0, c.stream>>>(m, n, bits, err), note_launches(1);                \
+    break;
+  switch (dt) {
+    ADC_MASK_CASE(ADC_U8)
+    ADC_MASK_CASE(ADC_F32)
+    ADC_MASK_CASE(ADC_BF16)
+    ADC_MASK_CASE(ADC_F16)
+    default: return -1;
+  }
+#undef ADC_MASK_CASE
+  return 0;
+}
+
+int launch_mask_unpack(const Ctx &c, const uint8_t *bits, int64_t n, uint8_t *out) {
+  const bool fast = n % 8 == 0 && reinterpret_cast<uintptr_t>(out) % 8 == 0;
+  const int grid = grid_of(c, (n + 7) / 8);
+  if (fast)
+    mask_unpack<true><<<grid, kThreads, 0, c.stream>>>(bits, n, out), note_launches(1);
+  else
+    mask_unpack<false><<<grid, kThreads, 0, c.stream>>>(bits, n, out), note_launches(1);
+  return 0;
+}
+
+}  // namespace adc

@@ -69,3 +69,28 @@ def assert_matches_golden(name, golden, norm, deq):
     assert got.shape == want.shape and got.dtype == want.dtype, f"{name}/dequant: {got.shape}/{got.dtype}"
     # bitwise, so -0.0 vs +0.0 would be caught too
     np.testing.assert_array_equal(got.view(np.uint8), want.view(np.uint8), err_msg=f"{name}/dequant")
+
+
+def device_run(x, scheme, group, thr, *, in_dtype=None):
+    """CUDA path (through the C-ABI) -> (normalized dict, dequant f32) or error name."""
+    import torch
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200 import errors as E
+    t = torch.as_tensor(np.ascontiguousarray(x))
+    if in_dtype is not None:
+        t = t.to(in_dtype)
+    try:
+        ct = adc.compress(t, adc.SchemeSpec(adc.Scheme(scheme), group, thr))
+    except E.ActplanError as exc:
+        return type(exc).__name__, None
+    deq = adc.decompress(ct).cpu().numpy()
+    if scheme == cases.MASK:
+        norm = cases.normalized(None, None, None, None, None, ct.mask_bits.cpu().numpy())
+    else:
+        norm = cases.normalized(
+            ct.scales.cpu().numpy(),
+            None if ct.offsets is None else ct.offsets.cpu().numpy(),
+            ct.packed_codes.cpu().numpy(),
+            None if ct.outlier_indices is None else ct.outlier_indices.cpu().numpy(),
+            None if ct.outlier_values is None else ct.outlier_values.cpu().numpy(), None)
+    return norm, deq

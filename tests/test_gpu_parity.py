@@ -1,0 +1,216 @@
+"""Parity of the CUDA path (through the C-ABI) with the reference.
+
+Bit-exact on codes, scales, offsets, outlier index sets and outlier values;
+bit-exact on the float32 decompression (dequantisation is one
+rounding of an exact product, so float32 equality is achievable and tested
+bitwise).  Evidence layers:
+  * small_golden.npz -- reference outputs of KATs, 240 ragged random cases and
+    the adversarial asymmetric tie families;
+  * digests.json     -- reference digests of config-1 tensors (5 seeds x 4
+    codecs), Llama-shaped 4096^2 and acceptance gates 2 and 9;
+  * the oracle       -- on bf16 / f16 inputs, big-magnitude sums (>= 2^29,
+    numpy's sequential order matters) and full BASELINE-size tensors.
+"""
+
+import numpy as np
+import pytest
+
+import cases
+from _harness import (assert_matches_golden, device_run, load_digests, load_small, oracle_run,
+                      small_inputs)
+
+pytestmark = pytest.mark.gpu
+
+SMALL = load_small()
+INPUTS = small_inputs()
+DIGESTS = load_digests()
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    torch.cuda.init()
+    return torch
+
+
+@pytest.mark.parametrize("name", sorted(SMALL))
+def test_small_golden(torch_cuda, name):
+    x, s, g, t = INPUTS[name]
+    norm, deq = device_run(x, s, g, t)
+    assert_matches_golden(name, SMALL[name], norm, deq)
+
+
+@pytest.mark.parametrize("key", sorted(k for k in DIGESTS if k.startswith("config1/")))
+def test_config1_digest(torch_cuda, key):
+    _, s, g, seed = key.split("/")
+    scheme, group, seed = int(s[1:]), int(g[1:]), int(seed[4:])
+    x = cases.config1_input(scheme, seed)
+    norm, deq = device_run(x, scheme, group, 3.0)
+    assert not isinstance(norm, str), norm
+    assert cases.norm_digest(norm, deq) == DIGESTS[key]
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_llama_digest(torch_cuda, seed):
+    x = cases.llama_input(seed)
+    for dt in (None, torch_cuda.bfloat16):   # the input is bf16-valued: both dtypes must agree
+        norm, deq = device_run(x, cases.OUTL, 128, 3.0, in_dtype=dt)
+        assert norm["idx"].size == DIGESTS[f"llama4096/outl/seed{seed}/k"]
+        assert cases.norm_digest(norm, deq) == DIGESTS[f"llama4096/outl/seed{seed}"]
+
+
+def test_gate2_digests(torch_cuda):
+    parts = {"sym16": [], "asym16": [], "pc": [], "outl16": [], "mask": []}
+    for x, hot, mask in cases.gate2_inputs():
+        for key, (arr, s, g) in {
+            "sym16": (x, cases.SYM, 16), "asym16": (x, cases.ASYM, 16),
+            "pc": (x, cases.SYM, cases.PER_CHANNEL), "outl16": (hot, cases.OUTL, 16),
+            "mask": (mask, cases.MASK, 0),
+        }.items():
+            norm, deq = device_run(arr, s, g, 3.0)
+            parts[key].append(cases.norm_digest(norm, deq))
+    for key, lst in parts.items():
+        assert cases.digest(np.array(lst)) == DIGESTS[f"gate2/{key}"], key
+
+
+def test_gate9_digest(torch_cuda):
+    import paper_2508_00806_b200 as adc
+    flagged = [",".join(str(i) for i in adc.detect_outlier_channels(x).cpu().tolist())
+               for x in cases.gate9_inputs()]
+    assert cases.digest(np.array(flagged)) == DIGESTS["gate9/flagged"]
+
+
+@pytest.mark.parametrize("dtype_name", ["bfloat16", "float16"])
+@pytest.mark.parametrize("scheme,group", [(0, 128), (0, 0), (1, 128), (2, 128), (0, 64), (1, 32)])
+def test_half_inputs_vs_oracle(torch_cuda, dtype_name, scheme, group):
+    """bf16/f16 activations: the oracle sees the same values as float32."""
+    torch = torch_cuda
+    dt = getattr(torch, dtype_name)
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=(512, 1024)).astype(np.float32)
+    x[:, rng.choice(1024, 6, replace=False)] *= 40.0
+    xt = torch.from_numpy(x).to(dt)
+    x_exact = xt.to(torch.float32).numpy()
+    want = oracle_run(x_exact, scheme, group, 3.0)
+    got = device_run(xt, scheme, group, 3.0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
+
+
+def test_big_sums_sequential_order(torch_cuda):
+    """Column |x|-sums >= 2^29: numpy's row order decides rounding (sequential fallback)."""
+    rng = np.random.default_rng(3)
+    x = (rng.uniform(40000, 65000, size=(16384, 64)) * rng.choice([-1, 1], size=(16384, 64))).astype(np.float32)
+    x[:, 5] = 65504.0
+    x[:, 9] *= 0.001
+    want = oracle_run(x, cases.OUTL, 128, 1.0)
+    got = device_run(x, cases.OUTL, 128, 1.0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
+    import paper_2508_00806_b200 as adc
+    from oracle import codec_oracle as orc
+    sums = adc.channel_abs_sums(x).cpu().numpy()
+    np.testing.assert_array_equal(sums.view(np.uint64),
+                                  orc.column_abs_sums(orc.to_f16_matrix(x)).view(np.uint64))
+
+
+@pytest.mark.parametrize("shape,scheme,group", [
+    ((8192, 1024), 2, 128), ((8192, 3072), 0, 0), ((8192, 4096), 2, 128),
+    ((16384, 1024), 1, 128), ((4096, 11008), 2, 128), ((32768, 1024), 3, 0)])
+def test_baseline_sizes_vs_oracle(torch_cuda, shape, scheme, group):
+    """Full configs[1]/[2] tensor sizes, bf16, against the oracle on the same values."""
+    torch = torch_cuda
+    rng = np.random.default_rng(shape[0] + shape[1] + scheme)
+    if scheme == 3:
+        x = (rng.random(size=shape) < 0.9).astype(np.uint8)
+        xt = torch.from_numpy(x).to(torch.bool)
+        want = oracle_run(x, scheme, group, 3.0)
+    else:
+        x = rng.standard_normal(size=shape, dtype=np.float32)
+        if scheme == 1:
+            x = np.abs(x) * 3.0
+        hot = rng.choice(shape[1], max(1, shape[1] // 100), replace=False)
+        x[:, hot] *= 30.0
+        xt = torch.from_numpy(x).to(torch.bfloat16)
+        want = oracle_run(xt.to(torch.float32).numpy(), scheme, group, 3.0)
+    got = device_run(xt, scheme, group, 3.0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
+
+
+@pytest.mark.parametrize("out", ["bfloat16", "float16"])
+def test_reduced_precision_outputs(torch_cuda, out):
+    """Training-mode outputs are the float32 reconstruction rounded RNE."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    rng = np.random.default_rng(5)
+    x = torch.from_numpy(rng.normal(size=(1024, 768)).astype(np.float32)).cuda()
+    x[:, 3] *= 60
+    for spec in (adc.SchemeSpec(adc.Scheme.SYMMETRIC_GROUP), adc.SchemeSpec(adc.Scheme.SYMMETRIC_GROUP, 0),
+                 adc.SchemeSpec(adc.Scheme.ASYMMETRIC_GROUP), adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED)):
+        ct = adc.compress(x, spec)
+        f32 = adc.decompress(ct)
+        low = adc.decompress(ct, out_dtype=getattr(torch, out))
+        assert torch.equal(low, f32.to(getattr(torch, out)))
+
+
+def test_async_record_matches_parity_record(torch_cuda):
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    rng = np.random.default_rng(9)
+    x = torch.from_numpy(rng.normal(size=(2048, 1024)).astype(np.float32)).cuda().to(torch.bfloat16)
+    x[:, 17] *= 80
+    spec = adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED)
+    ref = adc.compress(x, spec)
+    ct = adc.compress_async(x, spec, k_cap=64)
+    out = torch.empty((2048, 1024), dtype=torch.bfloat16, device="cuda")
+    adc.decompress_into(ct, out)
+    torch.cuda.synchronize()
+    assert int(ct.k_dev[1]) == ref.outlier_count
+    assert torch.equal(out, adc.decompress(ref).to(torch.bfloat16))
+    assert torch.equal(ct.packed_codes, ref.packed_codes)
+
+
+def test_k_cap_overflow_is_reported(torch_cuda):
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    rng = np.random.default_rng(10)
+    x = torch.from_numpy(rng.normal(size=(256, 512)).astype(np.float32)).cuda()
+    x[:, :6] *= 100
+    ct = adc.compress_async(x, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), k_cap=2)
+    from paper_2508_00806_b200.errors import ERR_K_CAP
+    err, k = ct.k_dev.cpu().tolist()
+    assert k == 6 and (err & ERR_K_CAP)
+
+
+def test_errors_map_to_reference_types(torch_cuda):
+    import paper_2508_00806_b200 as adc
+    with pytest.raises(adc.NonFiniteInputError):
+        adc.quantize_symmetric(np.array([1.0, np.nan], np.float32))
+    with pytest.raises(adc.NonFiniteInputError):
+        adc.compress_outlier_separated(np.array([[1.0, 1e6], [2.0, 3.0]], np.float32))
+    with pytest.raises(adc.TooManyOutliersError):
+        adc.compress_outlier_separated(np.array([[1000.0, 1000.0, 1.0]] * 4, np.float32), threshold=0.1)
+    with pytest.raises(adc.NonBinaryMaskError):
+        adc.pack_bitmask(np.array([0, 2, 1], np.uint8))
+    with pytest.raises(adc.ValidationError):
+        adc.quantize_symmetric(np.ones((2, 2, 2), np.float32))
+    with pytest.raises(adc.ValidationError):
+        adc.quantize_symmetric(np.ones(8, np.float32), group_size=-2)
+
+
+@pytest.mark.parametrize("spec_args", [(0, 128), (0, 0), (1, 32), (2, 128), (3, 0)])
+def test_wire_format_matches_oracle_bytes(torch_cuda, spec_args):
+    """serialize(device record) == the oracle's ADC1 bytes; deserialize round-trips."""
+    import paper_2508_00806_b200 as adc
+    from oracle import codec_oracle as orc
+    s, g = spec_args
+    rng = np.random.default_rng(6)
+    x = rng.normal(size=(16, 256)).astype(np.float32)
+    if s == 3:
+        x = (x > 0).astype(np.float32)
+    if s == 2:
+        x[:, 17] *= 90.0
+    ct = adc.compress(x, adc.SchemeSpec(adc.Scheme(s), g))
+    blob = adc.serialize(ct)
+    assert blob == orc.serialize(orc.compress(x, s, g))
+    back = adc.deserialize(blob)
+    assert adc.serialize(back) == blob
+    assert np.array_equal(adc.decompress(back).cpu().numpy(), adc.decompress(ct).cpu().numpy())
