@@ -142,6 +142,15 @@ __device__ __forceinline__ uint32_t f16_key2(uint32_t b) {
   return (b ^ (neg | 0x80008000u));
 }
 
+__device__ __forceinline__ uint32_t hmax2_nan(uint32_t a, uint32_t b) {
+  __half2 r = __hmax2_nan(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
+  return *reinterpret_cast<uint32_t *>(&r);
+}
+__device__ __forceinline__ uint32_t hmin2_nan(uint32_t a, uint32_t b) {
+  __half2 r = __hmin2_nan(*reinterpret_cast<__half2 *>(&a), *reinterpret_cast<__half2 *>(&b));
+  return *reinterpret_cast<uint32_t *>(&r);
+}
+
 __device__ __forceinline__ float h2f(uint32_t bits16) {
   return __half2float(__ushort_as_half(static_cast<uint16_t>(bits16)));
 }
@@ -205,10 +214,13 @@ __device__ __forceinline__ int sym_code(float h, const QParams &q) {
   return __float_as_int(r1 + kMagic) - 0x4B400000;
 }
 
-// Asymmetric code: d = f32(h - o) can round, but RN is monotone and every
-// decision boundary (k+1/2)*s is an f32 value, so a non-tie quotient lands on
-// the correct side; an exact half-integer quotient is re-done in float64
-// (codec.py:223-231 semantics), which is the rare slow path.
+// Asymmetric code.  d = f32(h - o) can round (tiny h against a large offset:
+// the Appendix A.5 KAT), so exactness is not available in f32.  Instead:
+// r = f32(d * inv) is within ~3 ulp, i.e. < 2^-19 absolute for |r| <= 9, of
+// the exact quotient (h - o)/s.  If r is farther than 2^-18 from every
+// half-integer, rint(r) equals the reference's rint of the float64 quotient;
+// otherwise (exact ties and near-ties, ~1e-5 of random elements) the code is
+// recomputed exactly in float64 exactly as codec.py:223-231 does.
 static __device__ __noinline__ int asym_code_f64(float h, const QParams &q) {
   double d = static_cast<double>(h) - static_cast<double>(q.o);
   double r = rint(d / static_cast<double>(q.s));
@@ -217,14 +229,11 @@ static __device__ __noinline__ int asym_code_f64(float h, const QParams &q) {
 }
 
 __device__ __forceinline__ int asym_code(float h, const QParams &q) {
-  float d = h - q.o;
-  float r0 = d * q.inv;
-  float rem = fmaf(-r0, q.s, d);
-  float r1 = fmaf(rem, q.inv, r0);
-  float c = (r1 + kMagic) - kMagic;
-  if (fabsf(r1 - c) == 0.5f) return asym_code_f64(h, q);
-  c = fminf(fmaxf(c, -8.f), 7.f);
-  return static_cast<int>(c);
+  const float d = h - q.o;
+  const float r = fminf(fmaxf(d * q.inv, -8.f), 7.f);
+  const float t = r + kMagic;
+  if (fabsf(r - (t - kMagic)) > 0.5f - 0x1p-18f) return asym_code_f64(h, q);
+  return __float_as_int(t) - 0x4B400000;
 }
 
 template <bool ASYM>

@@ -87,14 +87,21 @@ __global__ void __launch_bounds__(kThreads)
       uint16_t s_bits, o_bits = 0;
       bool bad;
       if (ASYM) {
-        uint32_t kx0 = f16_key2(h[k].x), kx1 = f16_key2(h[k].y);
-        uint32_t kx2 = f16_key2(h[k].z), kx3 = f16_key2(h[k].w);
-        uint32_t kmax = act ? __vmaxu2(__vmaxu2(kx0, kx1), __vmaxu2(kx2, kx3)) : 0u;
-        uint32_t kmin = act ? __vminu2(__vminu2(kx0, kx1), __vminu2(kx2, kx3)) : 0xffffffffu;
-        kmax = warp_max_u2<L>(kmax);
-        kmin = warp_min_u2<L>(kmin);
-        uint32_t hi = f16_unkey(max(kmax & 0xffffu, kmax >> 16));
-        uint32_t lo = f16_unkey(min(kmin & 0xffffu, kmin >> 16));
+        // packed f16x2 max/min; the _nan forms propagate NaN so the
+        // finiteness check below sees it
+        uint32_t vmax = 0xFC00FC00u, vmin = 0x7C007C00u;  // -inf / +inf: neutral
+        if (act) {
+          vmax = hmax2_nan(hmax2_nan(h[k].x, h[k].y), hmax2_nan(h[k].z, h[k].w));
+          vmin = hmin2_nan(hmin2_nan(h[k].x, h[k].y), hmin2_nan(h[k].z, h[k].w));
+        }
+#pragma unroll
+        for (int o = 1; o < L; o <<= 1) {
+          vmax = hmax2_nan(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+          vmin = hmin2_nan(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+        }
+        vmax = hmax2_nan(vmax, __funnelshift_l(vmax, vmax, 16));
+        vmin = hmin2_nan(vmin, __funnelshift_l(vmin, vmin, 16));
+        const uint32_t hi = vmax & 0xffffu, lo = vmin & 0xffffu;
         bad = ((hi & 0x7fffu) >= 0x7c00u) || ((lo & 0x7fffu) >= 0x7c00u);
         asym_params(hi, lo, o_bits, s_bits);
       } else {

@@ -119,37 +119,58 @@ __device__ double leaf_sum(const Term &t, int64_t lo, int64_t n) {
   return res;
 }
 
-// Leaves of the recursion, left to right (iterative DFS).
-__device__ int64_t enumerate_leaves(int64_t n, int64_t *leaf) {
-  int64_t stack_lo[64], stack_n[64];
+// The recursion of pairwise_sum_DOUBLE is evaluated without device recursion
+// (no dynamic stack): thread 0 walks the tree with explicit shared-memory
+// stacks, first to list the leaves left to right, later to add the leaf sums
+// back up in exactly the recursion's order.
+constexpr int kStackCap = 160;  // >= 2*depth+2; depth <= log2(n/57) < 64 for any int64 n
+
+__device__ int64_t enumerate_leaves(int64_t n, int64_t *leaf, int64_t *st_lo, int64_t *st_n) {
   int sp = 0;
   int64_t count = 0;
-  stack_lo[sp] = 0;
-  stack_n[sp++] = n;
+  st_lo[sp] = 0;
+  st_n[sp++] = n;
   while (sp) {
-    const int64_t lo = stack_lo[--sp], m = stack_n[sp];
+    --sp;
+    const int64_t lo = st_lo[sp], m = st_n[sp];
     if (m <= kBlock) {
       leaf[count++] = (lo << 8) | m;
       continue;
     }
     int64_t h = m / 2;
     h -= h % 8;
-    // push right first so the left subtree is visited first
-    stack_lo[sp] = lo + h;
-    stack_n[sp++] = m - h;
-    stack_lo[sp] = lo;
-    stack_n[sp++] = h;
+    st_lo[sp] = lo + h;  // right pushed first: the left subtree is visited first
+    st_n[sp++] = m - h;
+    st_lo[sp] = lo;
+    st_n[sp++] = h;
   }
   return count;
 }
 
-__device__ __noinline__ double combine(int64_t n, const double *leafsum, int64_t &li) {
-  if (n <= kBlock) return leafsum[li++];
-  int64_t h = n / 2;
-  h -= h % 8;
-  const double a = combine(h, leafsum, li);
-  const double b = combine(n - h, leafsum, li);
-  return __dadd_rn(a, b);
+// Post-order evaluation: node entries are n (to expand) or -1 (combine marker).
+__device__ double combine_tree(int64_t n, const double *leafsum, int64_t *st_n, double *vals) {
+  int sp = 0, vp = 0;
+  int64_t li = 0;
+  st_n[sp++] = n;
+  while (sp) {
+    const int64_t m = st_n[--sp];
+    if (m < 0) {
+      const double b = vals[--vp];
+      const double a = vals[--vp];
+      vals[vp++] = __dadd_rn(a, b);
+      continue;
+    }
+    if (m <= kBlock) {
+      vals[vp++] = leafsum[li++];
+      continue;
+    }
+    int64_t h = m / 2;
+    h -= h % 8;
+    st_n[sp++] = -1;
+    st_n[sp++] = m - h;
+    st_n[sp++] = h;
+  }
+  return vals[0];
 }
 
 constexpr int kStatsThreads = 1024;
@@ -163,9 +184,11 @@ __global__ void __launch_bounds__(kStatsThreads)
   __shared__ double s_mean, s_sigma;
   __shared__ int s_bad;
   __shared__ int64_t s_warp[kStatsThreads / 32];
+  __shared__ int64_t st_a[kStackCap], st_b[kStackCap];
+  __shared__ double st_v[kStackCap];
   const int tid = threadIdx.x;
   if (tid == 0) {
-    s_nleaves = enumerate_leaves(cols, leaf);
+    s_nleaves = enumerate_leaves(cols, leaf, st_a, st_b);
     s_bad = 0;
   }
   __syncthreads();
@@ -179,8 +202,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     leafsum[l] = leaf_sum(t, leaf[l] >> 8, leaf[l] & 0xff);
   __syncthreads();
   if (tid == 0) {
-    int64_t li = 0;
-    const double tot = __dadd_rn(0.0, combine(cols, leafsum, li));
+    const double tot = __dadd_rn(0.0, combine_tree(cols, leafsum, st_a, st_v));
     s_mean = __ddiv_rn(tot, static_cast<double>(cols));
   }
   __syncthreads();
@@ -190,8 +212,7 @@ __global__ void __launch_bounds__(kStatsThreads)
     leafsum[l] = leaf_sum(t, leaf[l] >> 8, leaf[l] & 0xff);
   __syncthreads();
   if (tid == 0) {
-    int64_t li = 0;
-    const double tot = __dadd_rn(0.0, combine(cols, leafsum, li));
+    const double tot = __dadd_rn(0.0, combine_tree(cols, leafsum, st_a, st_v));
     s_sigma = __dsqrt_rn(__ddiv_rn(tot, static_cast<double>(cols)));
     if (s_bad && err) atomicOr(err, ADC_ERR_NONFINITE);
   }

@@ -76,7 +76,7 @@ def device_run(x, scheme, group, thr, *, in_dtype=None):
     import torch
     import paper_2508_00806_b200 as adc
     from paper_2508_00806_b200 import errors as E
-    t = torch.as_tensor(np.ascontiguousarray(x))
+    t = x if isinstance(x, torch.Tensor) else torch.as_tensor(np.ascontiguousarray(x))
     if in_dtype is not None:
         t = t.to(in_dtype)
     try:
