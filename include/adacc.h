@@ -7,7 +7,10 @@
  *
  *   - All array arguments are DEVICE pointers owned by the caller; the library
  *     never allocates.  `workspace` is caller-owned scratch of
- *     adc_workspace_bytes() bytes (256-byte aligned).
+ *     adc_workspace_bytes() bytes (256-byte aligned) that must be zero-filled
+ *     once before its first use; every call leaves its counters at zero
+ *     again, so a workspace is reusable by stream-ordered calls without
+ *     re-clearing (the cross-CTA arrival counters live there).
  *   - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t
  *     passed as void*; NULL = legacy default stream).  Return value is a
  *     synchronous status: ADC_OK, ADC_EINVAL (argument validation, the

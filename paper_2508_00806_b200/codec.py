@@ -270,7 +270,7 @@ def compress_async(x: torch.Tensor, spec: SchemeSpec, *, k_cap: int | None = Non
     ws_bytes = 0
     if scheme is Scheme.OUTLIER_SEPARATED or spec.group_size == PER_CHANNEL:
         ws_bytes = _lib.lib().adc_workspace_bytes(int(scheme), rows, cols, spec.group_size)
-        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=dev)
     st = _lib.lib().adc_compress(
         int(scheme), x.data_ptr(), _DT[x.dtype], rows, cols, spec.group_size,
         float(spec.z_threshold), kc, codes.data_ptr(), scales.data_ptr(), _ptr(offsets),
@@ -435,7 +435,7 @@ def channel_abs_sums(x) -> torch.Tensor:
     t = _as_device_matrix(x)
     rows, cols = t.shape
     ws_bytes = _lib.lib().adc_workspace_bytes(int(Scheme.OUTLIER_SEPARATED), rows, cols, 0)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=t.device)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=t.device)
     sums = torch.empty(cols, dtype=torch.float64, device=t.device)
     status = torch.zeros(2, dtype=torch.int32, device=t.device)
     st = _lib.lib().adc_channel_abs_sums(t.data_ptr(), _DT[t.dtype], rows, cols, sums.data_ptr(),
@@ -449,7 +449,7 @@ def detect_outlier_channels(x, threshold: float = DEFAULT_Z_THRESHOLD) -> torch.
     t = _as_device_matrix(x)
     rows, cols = t.shape
     ws_bytes = _lib.lib().adc_workspace_bytes(int(Scheme.OUTLIER_SEPARATED), rows, cols, 0)
-    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=t.device)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=t.device)
     idx = torch.empty(cols, dtype=torch.int32, device=t.device)
     status = torch.zeros(2, dtype=torch.int32, device=t.device)
     st = _lib.lib().adc_detect_outliers(t.data_ptr(), _DT[t.dtype], rows, cols, float(threshold),

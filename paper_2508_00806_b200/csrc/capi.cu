@@ -45,7 +45,7 @@ static int sm_count() {
 
 static inline size_t up256(size_t v) { return (v + 255) & ~size_t(255); }
 
-static int64_t leaf_capacity(int64_t cols) { return cols / 32 + 8; }
+static int64_t node_capacity(int64_t cols) { return cols / 16 + 64; }
 
 size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   char *p = static_cast<char *>(base);
@@ -56,13 +56,18 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
     return r;
   };
   Workspace w;
+  const int64_t nodes = node_capacity(cols);
+  w.n_strips = static_cast<int>((cols + 255) / 256);
+  w.counters = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * (w.n_strips + 4)));
   w.colsum = reinterpret_cast<double *>(take(sizeof(double) * cols));
   w.colmax = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.flag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
   w.rank = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * cols));
-  w.leaf = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * leaf_capacity(cols)));
-  w.leafsum = reinterpret_cast<double *>(take(sizeof(double) * leaf_capacity(cols)));
-  w.misc = reinterpret_cast<uint32_t *>(take(64));
+  w.node_lo = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * nodes));
+  w.node_n = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * nodes));
+  w.node_left = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
+  w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
+  w.partial = reinterpret_cast<double *>(take(sizeof(double) * kMaxRowBlocks * cols));
   w.bytes = off;
   if (ws) *ws = w;
   return off;
@@ -145,11 +150,8 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
       return fail(ADC_EWORKSPACE, "workspace too small");
     Workspace ws;
     workspace_layout(cols, &ws, workspace);
-    if (cudaMemsetAsync(ws.flag, 0, static_cast<size_t>(cols) + 8, c.stream) != cudaSuccess)
-      return check_launch("memset");
-    rc |= launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
-    rc |= launch_outlier_stats(c, rows, cols, z_threshold, k_cap, ws, outlier_idx, k_out, err_word,
-                               true);
+    rc |= launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap,
+                              outlier_idx, k_out, err_word, true);
     rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag, ws.rank,
                                 outlier_idx, k_out, outlier_val, k_cap, codes, scales, nullptr,
                                 err_word);
@@ -217,8 +219,11 @@ int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols
   Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
   Workspace ws;
   workspace_layout(cols, &ws, workspace);
-  launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
-  launch_copy_sums(c, ws, sums, cols);
+  launch_colstats_sum(c, x, in_dtype, rows, cols, ws, false, 0.0, 0, nullptr, nullptr, err_word,
+                      false);
+  if (cudaMemcpyAsync(sums, ws.colsum, sizeof(double) * cols, cudaMemcpyDeviceToDevice, c.stream) !=
+      cudaSuccess)
+    return check_launch("channel_abs_sums copy");
   return check_launch("channel_abs_sums");
 }
 
@@ -234,10 +239,8 @@ int adc_detect_outliers(const void *x, int in_dtype, int64_t rows, int64_t cols,
   Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
   Workspace ws;
   workspace_layout(cols, &ws, workspace);
-  if (cudaMemsetAsync(ws.flag, 0, static_cast<size_t>(cols) + 8, c.stream) != cudaSuccess)
-    return check_launch("memset");
-  launch_colsum(c, x, in_dtype, rows, cols, ws, err_word);
-  launch_outlier_stats(c, rows, cols, z_threshold, k_cap, ws, outlier_idx, k_out, err_word, false);
+  launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap, outlier_idx, k_out,
+                      err_word, false);
   return check_launch("detect_outliers");
 }
 

@@ -5,8 +5,9 @@
 // packed COLUMN-major, i.e. nibble index c*rows + r (codec.py:232-233).
 //
 // Two kernels:
-//   channel_absmax  -- one read of x (kept in L2 with evict_last), per-column
-//                      abs-max as f16 bit patterns, atomicMax into workspace;
+//   colstats<MAX>   -- (outlier.cu) one read of x (kept in L2 with evict_last),
+//                      per-column abs-max as f16 bit patterns via per-CTA
+//                      partials and a last-CTA-per-strip reduction;
 //   channel_quant   -- re-reads x (L2-resident for activation-sized tensors),
 //                      quantises a 64-column x 256-row block with 8 column
 //                      scales held in registers, transposes row-major codes
@@ -24,44 +25,6 @@ constexpr int kTileCols = 64;     // 8 column units of 8
 constexpr int kSubRows = 64;      // rows per sub-tile (32 row pairs)
 constexpr int kBlockRows = 256;   // rows per block (4 sub-tiles)
 constexpr int kWordStride = 9;    // padded smem stride (words) per column
-
-template <int DT>
-__global__ void __launch_bounds__(kThreads)
-    channel_absmax(const void *__restrict__ x, int64_t rows, int64_t cols,
-                   uint32_t *__restrict__ colmax, uint32_t *__restrict__ err) {
-  __shared__ uint32_t red[8][32][4];
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t cu = static_cast<int64_t>(blockIdx.x) * 32 + tx;  // column unit
-  const bool live = cu * 8 < cols;
-  uint32_t m[4] = {0, 0, 0, 0};
-  if (live) {
-    for (int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + ty; r < rows;
-         r += static_cast<int64_t>(gridDim.y) * 8) {
-      uint4 h = Loader<DT>::template load8<true>(x, r * cols + cu * 8);
-      m[0] = __vmaxu2(m[0], h.x & 0x7fff7fffu);
-      m[1] = __vmaxu2(m[1], h.y & 0x7fff7fffu);
-      m[2] = __vmaxu2(m[2], h.z & 0x7fff7fffu);
-      m[3] = __vmaxu2(m[3], h.w & 0x7fff7fffu);
-    }
-  }
-#pragma unroll
-  for (int j = 0; j < 4; ++j) red[ty][tx][j] = m[j];
-  __syncthreads();
-  if (ty == 0 && live) {
-    bool bad = false;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      uint32_t v = red[0][tx][j];
-#pragma unroll
-      for (int t = 1; t < 8; ++t) v = __vmaxu2(v, red[t][tx][j]);
-      uint32_t lo = v & 0xffffu, hi = v >> 16;
-      bad |= lo >= 0x7c00u || hi >= 0x7c00u;
-      atomicMax(colmax + cu * 8 + 2 * j, lo);
-      atomicMax(colmax + cu * 8 + 2 * j + 1, hi);
-    }
-    if (bad) raise_err(err, ADC_ERR_NONFINITE);
-  }
-}
 
 // Byte `b` of word w.
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int b) { return (w >> (8 * b)) & 0xffu; }
@@ -227,15 +190,10 @@ bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *code
 int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
                             const Workspace &ws, uint8_t *codes, uint16_t *scales,
                             uint32_t *err) {
-  if (cudaMemsetAsync(ws.colmax, 0, sizeof(uint32_t) * cols, c.stream) != cudaSuccess) return -2;
-  dim3 ga(static_cast<unsigned>((cols / 8 + 31) / 32), 1);
-  int64_t want = static_cast<int64_t>(c.num_sms) * 8 / ga.x;
-  int64_t maxy = (rows + 7) / 8;
-  ga.y = static_cast<unsigned>(want < 1 ? 1 : (want > maxy ? maxy : want));
+  if (launch_colstats_max(c, x, dt, rows, cols, ws, err)) return -1;
   dim3 gq(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
           static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
   ADC_DT_SWITCH(dt, DT, {
-    channel_absmax<DT><<<ga, kThreads, 0, c.stream>>>(x, rows, cols, ws.colmax, err), note_launches(1);
     channel_quant<DT><<<gq, kThreads, 0, c.stream>>>(x, rows, cols, ws.colmax, codes, scales), note_launches(1);
   });
   return 0;

@@ -31,15 +31,21 @@ struct Ctx {
   int num_sms;
 };
 
-// Workspace carving (offsets in bytes, 256-aligned).
+// Workspace carving (offsets in bytes, 256-aligned).  Must be zero-filled
+// once by the caller; the kernels leave every counter at zero on exit.
+constexpr int kMaxRowBlocks = 128;  // gy cap of the column-statistics kernel
 struct Workspace {
-  double *colsum;        // cols       (outlier)
-  uint32_t *colmax;      // cols       (per-channel abs-max bits)
-  uint8_t *flag;         // cols       (outlier flags, padded to 8)
-  int32_t *rank;         // cols       (outlier rank of a flagged column, else -1)
-  int64_t *leaf;         // leaf table for the pairwise tree (start<<20 | len)
-  double *leafsum;       // per-leaf partial sums
-  uint32_t *misc;        // [0] inexact-sum flag, [1] leaf count
+  double *colsum;        // cols       column |x| sums (outlier)
+  uint32_t *colmax;      // cols       column abs-max f16 bits (per-channel)
+  uint8_t *flag;         // cols + 8   outlier flags
+  int32_t *rank;         // cols       outlier rank of a flagged column, else -1
+  double *partial;       // kMaxRowBlocks * cols per-CTA column partials
+  uint32_t *counters;    // n_strips + 4 arrival counters / flags
+  int n_strips;
+  int64_t *node_lo;      // pairwise-tree nodes
+  int64_t *node_n;
+  int32_t *node_left;
+  double *node_val;
   size_t bytes;
 };
 
@@ -71,13 +77,12 @@ int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, i
 int launch_channel_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
                               int64_t rows, int64_t cols, void *y, int ot);
 
-// outlier detection (outlier.cu)
-int launch_colsum(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                  const Workspace &ws, uint32_t *err);
-int launch_outlier_stats(const Ctx &c, int64_t rows, int64_t cols, double thr, int64_t k_cap,
-                         const Workspace &ws, uint32_t *idx, int32_t *k_out, uint32_t *err,
-                         bool too_many_check);
-int launch_copy_sums(const Ctx &c, const Workspace &ws, double *out, int64_t cols);
+// column statistics (outlier.cu): one launch each
+int launch_colstats_sum(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                        const Workspace &ws, bool do_stats, double thr, int64_t k_cap,
+                        uint32_t *idx, int32_t *k_out, uint32_t *err, bool too_many_check);
+int launch_colstats_max(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                        const Workspace &ws, uint32_t *err);
 
 // masks (mask.cu)
 int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bits,

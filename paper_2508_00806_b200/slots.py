@@ -55,7 +55,7 @@ class CodecSlot:
         if self.scheme is Scheme.OUTLIER_SEPARATED or (self.scheme is not Scheme.BIT_MASK
                                                        and g == PER_CHANNEL):
             self.ws_bytes = _lib.lib().adc_workspace_bytes(int(self.scheme), self.rows, self.cols, g)
-            self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+            self.ws = torch.zeros(self.ws_bytes, dtype=torch.uint8, device=dev)
         p = lambda t: None if t is None else t.data_ptr()  # noqa: E731
         self._c_args = (int(self.scheme), _IN[in_dtype], self.rows, self.cols, g,
                         float(spec.z_threshold), self.k_cap, p(self.codes), p(self.scales),
