@@ -63,8 +63,8 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   w.colmax = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.flag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
   w.rank = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * cols));
-  w.node_lo = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * nodes));
-  w.node_n = reinterpret_cast<int64_t *>(take(sizeof(int64_t) * nodes));
+  w.node_lo = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
+  w.node_n = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_left = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
   w.partial = reinterpret_cast<double *>(take(sizeof(double) * kMaxRowBlocks * cols));

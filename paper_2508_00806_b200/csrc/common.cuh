@@ -190,16 +190,26 @@ struct QParams {
   float o;    // offset (0 for symmetric)
 };
 
+// MUFU.RCP, ~1 ulp.  A correctly rounded reciprocal is not needed: the
+// symmetric path refines the quotient with one Markstein step (exact on ties,
+// within 1 ulp elsewhere), the asymmetric path widens its near-tie window.
+__device__ __forceinline__ float rcp_approx(float v) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+  return r;
+}
+
 __device__ __forceinline__ QParams make_qparams(uint16_t s_bits, uint16_t o_bits) {
   QParams q;
   float s = h2f(s_bits);
   q.s = (s == 0.f) ? 1.f : s;
-  q.inv = __frcp_rn(q.s);
+  q.inv = rcp_approx(q.s);
   q.o = h2f(o_bits);
   return q;
 }
 
 constexpr float kMagic = 12582912.0f;  // 1.5 * 2^23: x + kMagic rounds to int, RNE
+constexpr float kMagic8 = 12582920.0f;  // kMagic + 8: low nibble of the sum = code + 8
 
 // Symmetric code of one element as an int in [-8, 7].
 // r1 is the correctly rounded f32 quotient h/s (Markstein: r0 = h*inv,
@@ -216,8 +226,9 @@ __device__ __forceinline__ int sym_code(float h, const QParams &q) {
 
 // Asymmetric code.  d = f32(h - o) can round (tiny h against a large offset:
 // the Appendix A.5 KAT), so exactness is not available in f32.  Instead:
-// r = f32(d * inv) is within ~3 ulp, i.e. < 2^-19 absolute for |r| <= 9, of
-// the exact quotient (h - o)/s.  If r is farther than 2^-18 from every
+// r = f32(d * inv) (inv = MUFU.RCP, ~1 ulp) is within ~4 ulp, i.e. < 2^-18.8
+// absolute for |r| <= 9, of the exact quotient (h - o)/s.  If r is farther
+// than 2^-17 from every
 // half-integer, rint(r) equals the reference's rint of the float64 quotient;
 // otherwise (exact ties and near-ties, ~1e-5 of random elements) the code is
 // recomputed exactly in float64 exactly as codec.py:223-231 does.
@@ -232,7 +243,7 @@ __device__ __forceinline__ int asym_code(float h, const QParams &q) {
   const float d = h - q.o;
   const float r = fminf(fmaxf(d * q.inv, -8.f), 7.f);
   const float t = r + kMagic;
-  if (fabsf(r - (t - kMagic)) > 0.5f - 0x1p-18f) return asym_code_f64(h, q);
+  if (fabsf(r - (t - kMagic)) > 0.5f - 0x1p-17f) return asym_code_f64(h, q);
   return __float_as_int(t) - 0x4B400000;
 }
 
@@ -256,6 +267,45 @@ __device__ __forceinline__ uint32_t quant_pack8(uint4 h, const QParams &q) {
     out |= (static_cast<uint32_t>(c1) & 0xfu) << (8 * j + 4);
   }
   return out;
+}
+
+// ---- 16-elements-per-lane fast path helpers -------------------------------
+// "t-bits": the f32 bit pattern of r + kMagic8, whose low nibble is code + 8
+// and whose bits 4..21 are zero; packing works on these directly.
+//
+// Symmetric, normal scale (s >= 2^-14): |h/s| <= 8/(1 - 2^-11) < 8.004, so
+// rint never goes below -8 and only the upper clip is needed.
+__device__ __forceinline__ uint32_t sym_tbits(float h, float s, float inv) {
+  const float r0 = h * inv;
+  const float rem = fmaf(-r0, s, h);
+  const float r1 = fminf(fmaf(rem, inv, r0), 7.f);
+  return __float_as_uint(r1 + kMagic8);
+}
+// Subnormal (or zero -> 1) scale: the f16 rounding of top/8 can be coarse,
+// clip both ends (codec.py:231).
+__device__ __forceinline__ uint32_t sym_tbits_clip2(float h, float s, float inv) {
+  const float r0 = h * inv;
+  const float rem = fmaf(-r0, s, h);
+  const float r1 = fminf(fmaxf(fmaf(rem, inv, r0), -8.f), 7.f);
+  return __float_as_uint(r1 + kMagic8);
+}
+__device__ __forceinline__ uint32_t asym_tbits(float h, const QParams &q) {
+  const float d = h - q.o;
+  const float r = fminf(fmaxf(d * q.inv, -8.f), 7.f);
+  const float t = r + kMagic8;
+  if (fabsf(r - (t - kMagic8)) > 0.5f - 0x1p-17f)
+    return 0x4B400008u + static_cast<uint32_t>(asym_code_f64(h, q));
+  return __float_as_uint(t);
+}
+
+// Pack 8 t-bits (elements 0..7) into one word of nibbles, element 0 lowest
+// (codec.py:199-203): pairs by IMAD (hi*16 + lo keeps both nibbles in the low
+// byte), bytes gathered by PRMT, the +8 offset removed by one XOR.
+__device__ __forceinline__ uint32_t pack8_tbits(const uint32_t *t) {
+  const uint32_t p0 = t[1] * 16u + t[0], p1 = t[3] * 16u + t[2];
+  const uint32_t p2 = t[5] * 16u + t[4], p3 = t[7] * 16u + t[6];
+  const uint32_t a = __byte_perm(p0, p1, 0x0040), b = __byte_perm(p2, p3, 0x0040);
+  return __byte_perm(a, b, 0x5410) ^ 0x88888888u;
 }
 
 // Signed code of nibble j of a packed word.
@@ -323,6 +373,45 @@ struct Storer<ADC_F16> {
     static_cast<__half *>(y)[i] = __float2half_rn(v);
   }
 };
+
+// ---------------------------------------------------------------------------
+// mbarrier + bulk-copy (TMA engine, 1-D) pipeline primitives
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_barrier_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_WAIT;\n\t}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy (UBLKCP), completion counted on `bar` in bytes;
+// evict-first: the source is streamed once.
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}"
+      ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
 
 __device__ __forceinline__ void raise_err(uint32_t *err, uint32_t bit) {
   if (err) atomicOr(err, bit);

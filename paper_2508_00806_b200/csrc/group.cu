@@ -9,6 +9,8 @@
 // A group of g = 8*L elements is owned by L adjacent lanes of a warp and
 // reduced with L-wide xor shuffles; every lane derives the group's scale
 // itself (no broadcast), lane 0 of the group stores it.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -31,85 +33,190 @@ __device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
   return v;
 }
 
-// Zero the flagged channels of one unit (codec.py:328-329) and copy their
-// original f16 values into the (k, rows) side buffer (codec.py:340).  The
-// flag test is inline; the rare hit path is out of line to keep registers.
-__device__ __noinline__ void zero_outlier_hit(uint4 &h, uint2 f, uint32_t r, uint32_t c,
+// Zero the flagged channels of 8 consecutive elements (one row segment,
+// codec.py:328-329) and copy their original f16 values into the (k, rows)
+// side buffer (codec.py:340).  The flag test is inline; the rare hit path is
+// out of line to keep registers.
+__device__ __noinline__ void zero_outlier_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
                                               const int32_t *__restrict__ rank,
                                               uint16_t *__restrict__ outl_val, int64_t rows,
-                                              int64_t k_cap) {
-  uint32_t w[4] = {h.x, h.y, h.z, h.w};
+                                              int64_t k_cap, bool bf16_words) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     uint32_t fb = ((j < 4 ? f.x : f.y) >> (8 * (j & 3))) & 0xffu;
     if (fb) {
       uint32_t bits = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+      if (bf16_words) bits = __half_as_ushort(__float2half_rn(__uint_as_float(bits << 16)));
       int32_t rk = __ldg(rank + c + j);
       if (rk >= 0 && rk < k_cap) outl_val[static_cast<int64_t>(rk) * rows + r] = bits;
       w[j >> 1] &= (j & 1) ? 0x0000ffffu : 0xffff0000u;
     }
   }
-  h = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-__device__ __forceinline__ void zero_outlier_lanes(uint4 &h, int64_t e, const FastDiv &dc,
+__device__ __forceinline__ void zero_outlier_lanes(uint32_t *w, int64_t e, const FastDiv &dc,
                                                    const uint8_t *__restrict__ zflag,
                                                    const int32_t *__restrict__ rank,
                                                    uint16_t *__restrict__ outl_val, int64_t rows,
-                                                   int64_t k_cap) {
+                                                   int64_t k_cap, bool bf16_words) {
   uint32_t r = fastdiv(static_cast<uint32_t>(e), dc);
   uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
   uint2 f = __ldg(reinterpret_cast<const uint2 *>(zflag + c));
-  if ((f.x | f.y) != 0) zero_outlier_hit(h, f, r, c, rank, outl_val, rows, k_cap);
+  if ((f.x | f.y) != 0) zero_outlier_hit(w, f, r, c, rank, outl_val, rows, k_cap, bf16_words);
 }
 
-template <int DT, bool ASYM, int L, bool ZERO, int U>
-__global__ void __launch_bounds__(kThreads)
+__device__ __forceinline__ float lo_f(uint32_t w) {
+  return __low2float(*reinterpret_cast<const __half2 *>(&w));
+}
+__device__ __forceinline__ float hi_f(uint32_t w) {
+  return __high2float(*reinterpret_cast<const __half2 *>(&w));
+}
+
+// Raw-word element access.  bf16 inputs are quantised NATIVELY: every bf16
+// value with |x| >= 2^-17 is exactly representable in f16 (8-bit vs 11-bit
+// mantissa), so f16(x) == x and the per-element f32->f16->f32 round trip of
+// codec.py:158 is skipped.  Only groups whose scale could be affected by the
+// subnormal f16 rounding of tiny values take the converting path (see
+// below); f16 inputs need no conversion at all; f32 inputs are converted to
+// f16 on load.
+template <int DT>
+struct Raw {  // f16 words (F16, F32-converted)
+  static constexpr bool kBf16 = false;
+  template <bool KEEP>
+  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
+    return Loader<DT>::template load8<KEEP>(x, i);
+  }
+  __device__ __forceinline__ static float lo(uint32_t w) { return lo_f(w); }
+  __device__ __forceinline__ static float hi(uint32_t w) { return hi_f(w); }
+};
+template <>
+struct Raw<ADC_BF16> {
+  static constexpr bool kBf16 = true;
+  template <bool KEEP>
+  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
+    return Loader<ADC_F16>::template load8<KEEP>(x, i);  // raw 16-bit words
+  }
+  __device__ __forceinline__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
+  __device__ __forceinline__ static float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
+};
+
+__device__ __forceinline__ uint32_t bf16_bits_to_f16_bits(uint32_t b) {
+  return __half_as_ushort(__float2half_rn(__uint_as_float(b << 16)));
+}
+__device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
+  return *reinterpret_cast<uint32_t *>(&r);
+}
+__device__ __forceinline__ uint32_t bmin2_nan(uint32_t a, uint32_t b) {
+  __nv_bfloat162 r = __hmin2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
+  return *reinterpret_cast<uint32_t *>(&r);
+}
+
+// Exact (converting) element codes for one unit: h = f16(x), float64 quotient
+// as in codec.py:223-231.  Used for the rare groups / units the fast paths
+// cannot decide.
+template <bool BF16, int NW>
+__device__ __forceinline__ void unit_codes_exact(const uint32_t *w, float s, float o, bool asym,
+                                              uint32_t *t) {
+#pragma unroll
+  for (int i = 0; i < 2 * NW; ++i) {
+    const uint32_t raw = (w[i >> 1] >> (16 * (i & 1))) & 0xffffu;
+    const uint32_t hb = BF16 ? bf16_bits_to_f16_bits(raw) : raw;
+    const double h = static_cast<double>(h2f(hb));
+    const double sd = s == 0.f ? 1.0 : static_cast<double>(s);
+    double r = rint((asym ? h - static_cast<double>(o) : h) / sd);
+    r = fmin(fmax(r, -8.0), 7.0);
+    t[i] = 0x4B400008u + static_cast<uint32_t>(static_cast<int>(r));
+  }
+}
+
+// Fast group kernel: a lane owns EPL (8 or 16) consecutive elements, a group
+// of g = EPL*L elements is owned by L adjacent lanes; U units per lane are
+// loaded before any is processed (memory-level parallelism).
+template <int DT, bool ASYM, int L, bool ZERO, int EPL, int U>
+__global__ void __launch_bounds__(kThreads, 4)
     group_quant_fast(const void *__restrict__ x, int64_t n_units, int64_t n_units_pad, FastDiv dc,
                      int64_t rows, const uint8_t *__restrict__ zflag,
                      const int32_t *__restrict__ rank, uint16_t *__restrict__ outl_val,
                      int64_t k_cap, uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                      uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
+  constexpr int NW = EPL / 2;  // 16-bit pairs per unit
+  constexpr int NC = EPL / 8;  // packed code words per unit
+  using R = Raw<DT>;
+  constexpr bool BF = R::kBf16;
   const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units_pad;
        base += step) {
-    uint4 h[U];
+    uint32_t w[U][NW];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      int64_t u = base + k * kThreads + threadIdx.x;
-      h[k] = (u < n_units) ? Loader<DT>::template load8<false>(x, u * 8) : make_uint4(0, 0, 0, 0);
+      const int64_t u = base + k * kThreads + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (u < n_units) v = R::template load8<false>(x, u * EPL + 8 * q);
+        w[k][4 * q] = v.x;
+        w[k][4 * q + 1] = v.y;
+        w[k][4 * q + 2] = v.z;
+        w[k][4 * q + 3] = v.w;
+      }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t u = base + k * kThreads + threadIdx.x;
       const bool act = u < n_units;
-      if (ZERO && act) zero_outlier_lanes(h[k], u * 8, dc, zflag, rank, outl_val, rows, k_cap);
+      if (ZERO && act) {
+#pragma unroll
+        for (int q = 0; q < NC; ++q)
+          zero_outlier_lanes(&w[k][4 * q], u * EPL + 8 * q, dc, zflag, rank, outl_val, rows, k_cap,
+                             BF);
+      }
       uint16_t s_bits, o_bits = 0;
-      bool bad;
+      bool bad, native = true;
       if (ASYM) {
-        // packed f16x2 max/min; the _nan forms propagate NaN so the
-        // finiteness check below sees it
-        uint32_t vmax = 0xFC00FC00u, vmin = 0x7C007C00u;  // -inf / +inf: neutral
+        // packed max/min (NaN-propagating) in the input's own 16-bit format
+        uint32_t vmax = BF ? 0xFF80FF80u : 0xFC00FC00u, vmin = BF ? 0x7F807F80u : 0x7C007C00u;
         if (act) {
-          vmax = hmax2_nan(hmax2_nan(h[k].x, h[k].y), hmax2_nan(h[k].z, h[k].w));
-          vmin = hmin2_nan(hmin2_nan(h[k].x, h[k].y), hmin2_nan(h[k].z, h[k].w));
+          vmax = w[k][0];
+          vmin = w[k][0];
+#pragma unroll
+          for (int i = 1; i < NW; ++i) {
+            vmax = BF ? bmax2_nan(vmax, w[k][i]) : hmax2_nan(vmax, w[k][i]);
+            vmin = BF ? bmin2_nan(vmin, w[k][i]) : hmin2_nan(vmin, w[k][i]);
+          }
         }
 #pragma unroll
         for (int o = 1; o < L; o <<= 1) {
-          vmax = hmax2_nan(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-          vmin = hmin2_nan(vmin, __shfl_xor_sync(0xffffffffu, vmin, o));
+          const uint32_t a = __shfl_xor_sync(0xffffffffu, vmax, o), b = __shfl_xor_sync(0xffffffffu, vmin, o);
+          vmax = BF ? bmax2_nan(vmax, a) : hmax2_nan(vmax, a);
+          vmin = BF ? bmin2_nan(vmin, b) : hmin2_nan(vmin, b);
         }
-        vmax = hmax2_nan(vmax, __funnelshift_l(vmax, vmax, 16));
-        vmin = hmin2_nan(vmin, __funnelshift_l(vmin, vmin, 16));
-        const uint32_t hi = vmax & 0xffffu, lo = vmin & 0xffffu;
+        const uint32_t smax = __funnelshift_l(vmax, vmax, 16), smin = __funnelshift_l(vmin, vmin, 16);
+        vmax = BF ? bmax2_nan(vmax, smax) : hmax2_nan(vmax, smax);
+        vmin = BF ? bmin2_nan(vmin, smin) : hmin2_nan(vmin, smin);
+        uint32_t hi = vmax & 0xffffu, lo = vmin & 0xffffu;
+        if (BF) {
+          hi = bf16_bits_to_f16_bits(hi);  // f16 rounding is monotone: f16(max) = max(f16)
+          lo = bf16_bits_to_f16_bits(lo);
+        }
         bad = ((hi & 0x7fffu) >= 0x7c00u) || ((lo & 0x7fffu) >= 0x7c00u);
         asym_params(hi, lo, o_bits, s_bits);
       } else {
-        uint32_t m = act ? absmax8(h[k]) : 0u;
+        uint32_t m = 0;
+        if (act) {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) m = __vmaxu2(m, w[k][i] & 0x7fff7fffu);
+        }
         m = warp_max_u2<L>(m);
-        uint32_t top = max(m & 0xffffu, m >> 16);
-        bad = top >= 0x7c00u;
-        s_bits = sym_scale_bits(top);
+        const uint32_t top = max(m & 0xffffu, m >> 16);
+        if (BF) {
+          bad = top >= 0x4780u;       // >= 65536 rounds to f16 inf (also inf/NaN)
+          native = top >= 0x3900u;    // top >= 2^-13: scale >= 2^-16, tiny-value rounding is code-neutral
+          s_bits = sym_scale_bits(bf16_bits_to_f16_bits(top));
+        } else {
+          bad = top >= 0x7c00u;
+          s_bits = sym_scale_bits(top);
+        }
       }
       const int64_t grp = u / L;
       if ((threadIdx.x & (L - 1)) == 0 && u < n_units_pad) {
@@ -117,38 +224,90 @@ __global__ void __launch_bounds__(kThreads)
         scales[grp] = s_bits;
         if (ASYM) offsets[grp] = o_bits;
       }
-      if (act) {
-        QParams q = make_qparams(s_bits, o_bits);
-        codes[u] = quant_pack8<ASYM>(h[k], q);
+      if (!act) continue;
+      uint32_t t[EPL];
+      if (ASYM) {
+        const QParams q = make_qparams(s_bits, o_bits);
+        // r is within 2^-18.8 of the exact quotient of the f16 value; for bf16
+        // the native x differs from f16(x) by <= 2^-25 (tiny values only), i.e.
+        // by <= 2^-25/s in the quotient.  Units with any r inside that margin
+        // of a half-integer are redone exactly (branch per unit, not element).
+        const float margin = 0x1p-17f + (BF ? 0x1p-25f * q.inv : 0.f);
+        float worst = 0.f;
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const float xv = hh ? R::hi(w[k][i]) : R::lo(w[k][i]);
+            const float r = fminf(fmaxf((xv - q.o) * q.inv, -8.f), 7.f);
+            const float tv = r + kMagic8;
+            worst = fmaxf(worst, fabsf(r - (tv - kMagic8)));
+            t[2 * i + hh] = __float_as_uint(tv);
+          }
+        }
+        if (worst > 0.5f - margin) unit_codes_exact<BF, NW>(w[k], h2f(s_bits), q.o, true, t);
+      } else if (!BF || native) {
+        if (s_bits >= 0x0400u) {  // normal scale: upper clip only
+          const float sc = h2f(s_bits), inv = rcp_approx(sc);
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            t[2 * i] = sym_tbits(R::lo(w[k][i]), sc, inv);
+            t[2 * i + 1] = sym_tbits(R::hi(w[k][i]), sc, inv);
+          }
+        } else {
+          const float s0 = h2f(s_bits), sc = s0 == 0.f ? 1.f : s0, inv = rcp_approx(sc);
+#pragma unroll
+          for (int i = 0; i < NW; ++i) {
+            t[2 * i] = sym_tbits_clip2(R::lo(w[k][i]), sc, inv);
+            t[2 * i + 1] = sym_tbits_clip2(R::hi(w[k][i]), sc, inv);
+          }
+        }
+      } else {  // bf16 group with a tiny maximum: exact converting path
+        unit_codes_exact<BF, NW>(w[k], h2f(s_bits), 0.f, false, t);
+      }
+      if (NC == 1) {
+        codes[u] = pack8_tbits(t);
+      } else {
+        *reinterpret_cast<uint2 *>(codes + 2 * u) = make_uint2(pack8_tbits(t), pack8_tbits(t + 8));
       }
     }
   }
 }
 
-template <int OT, bool ASYM, int L, int U>
+template <int OT, bool ASYM, int L, int EPL, int U>
 __global__ void __launch_bounds__(kThreads)
     group_dequant_fast(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
                        const uint16_t *__restrict__ offsets, int64_t n_units, void *__restrict__ y) {
+  constexpr int NC = EPL / 8;
   const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units;
        base += step) {
-    uint32_t w[U];
+    uint32_t w[U][NC];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      int64_t u = base + k * kThreads + threadIdx.x;
-      w[k] = (u < n_units) ? __ldcs(codes + u) : 0u;
+      const int64_t u = base + k * kThreads + threadIdx.x;
+      if (NC == 1) {
+        w[k][0] = (u < n_units) ? __ldcs(codes + u) : 0u;
+      } else {
+        const uint2 v = (u < n_units) ? __ldcs(reinterpret_cast<const uint2 *>(codes) + u) : make_uint2(0, 0);
+        w[k][0] = v.x;
+        w[k][NC - 1] = v.y;
+      }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      int64_t u = base + k * kThreads + threadIdx.x;
+      const int64_t u = base + k * kThreads + threadIdx.x;
       if (u >= n_units) continue;
       const int64_t grp = u / L;
-      float s = h2f(__ldg(scales + grp));
-      float o = ASYM ? h2f(__ldg(offsets + grp)) : 0.f;
-      float v[8];
+      const float s = h2f(__ldg(scales + grp));
+      const float o = ASYM ? h2f(__ldg(offsets + grp)) : 0.f;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = deq<ASYM>(nib_code(w[k], j), s, o);
-      Storer<OT>::store8(y, u * 8, v);
+      for (int q = 0; q < NC; ++q) {
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = deq<ASYM>(nib_code(w[k][q], j), s, o);
+        Storer<OT>::store8(y, u * EPL + 8 * q, v);
+      }
     }
   }
 }
@@ -280,6 +439,15 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+bool use_tma_compress() {
+  static int v = -1;
+  if (v < 0) {
+    const char *e = getenv("ADC_COMPRESS_PATH");
+    v = (e && e[0] == 't') ? 1 : 0;  // measured: the register path is faster for now
+  }
+  return v == 1;
+}
+
 static inline int grid_for(const Ctx &c, int64_t work_items, int per_block) {
   int64_t need = (work_items + per_block - 1) / per_block;
   int64_t cap = static_cast<int64_t>(c.num_sms) * 8;
@@ -291,16 +459,11 @@ static inline bool aligned(const void *p, size_t a) {
   return (reinterpret_cast<uintptr_t>(p) % a) == 0;
 }
 
-static inline int lanes_for_group(int64_t g) {
-  switch (g) {
-    case 8: return 1;
-    case 16: return 2;
-    case 32: return 4;
-    case 64: return 8;
-    case 128: return 16;
-    case 256: return 32;
-    default: return 0;
-  }
+// Lanes per group for EPL elements per lane (0: no fast path).
+static inline int lanes_for_group(int64_t g, int epl) {
+  if (g < epl || g > 32 * epl || g % epl) return 0;
+  const int64_t l = g / epl;
+  return (l & (l - 1)) == 0 ? static_cast<int>(l) : 0;
 }
 
 #define ADC_DT_SWITCH(dt, DT, ...)                                   \
@@ -331,28 +494,53 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
                           uint32_t *err) {
   const int64_t n = rows * cols;
   const bool pc = (g == 0);
-  const int L = pc ? 0 : lanes_for_group(g);
   const bool zero = zero_flag != nullptr;
-  const bool fast = L > 0 && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) &&
-                    (!zero || (cols % 8 == 0 && n < (1ll << 31)));
-  if (fast) {
-    const int64_t n_units = n / 8;
-    const int64_t n_groups = (n_units + L - 1) / L;
-    const int64_t n_units_pad = n_groups * L;
-    const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
+  const bool zero_ok = !zero || (cols % 8 == 0 && n < (1ll << 31));
+  const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
+  int L = pc ? 0 : lanes_for_group(g, 8);
+  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok)
+    return launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, rank, outl_val,
+                                     k_cap, codes, scales, offsets, err);
+  L = pc ? 0 : lanes_for_group(g, 16);
+  if (L > 0 && n % 16 == 0 && aligned(x, 16) && aligned(codes, 8) && zero_ok) {
+    const int64_t n_units = n / 16;
+    const int64_t n_units_pad = (n_units + L - 1) / L * L;
     const int grid = grid_for(c, n_units_pad, kThreads * kUnroll);
     uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
-        group_quant_fast<DT, true, LL, false, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, true, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
             offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, false, LL, true, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, rows, zero_flag, rank, outl_val, k_cap, codes32, scales,
             nullptr, err), note_launches(1);
       } else {
-        group_quant_fast<DT, false, LL, false, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, false, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
+            nullptr, err), note_launches(1);
+      }
+    }));
+    return 0;
+  }
+  L = pc ? 0 : lanes_for_group(g, 8);
+  if (L > 0 && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok) {
+    const int64_t n_units = n / 8;
+    const int64_t n_units_pad = (n_units + L - 1) / L * L;
+    const int grid = grid_for(c, n_units_pad, kThreads * kUnroll);
+    uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
+    ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
+      if (asym) {
+        group_quant_fast<DT, true, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
+            offsets, err), note_launches(1);
+      } else if (zero) {
+        group_quant_fast<DT, false, LL, true, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, rows, zero_flag, rank, outl_val, k_cap, codes32, scales,
+            nullptr, err), note_launches(1);
+      } else {
+        group_quant_fast<DT, false, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
             nullptr, err), note_launches(1);
       }
@@ -405,18 +593,33 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
                             bool asym, void *y, int ot) {
   const int64_t n = rows * cols;
   const bool pc = (g == 0);
-  const int L = pc ? 0 : lanes_for_group(g);
-  const bool fast = L > 0 && n % 8 == 0 && aligned(y, 16) && aligned(codes, 4);
-  if (fast) {
+  // 8 elements per lane measured faster than 16 for the store-bound inverse
+  int L = pc ? 0 : lanes_for_group(g, 8);
+  if (L > 0 && n % 8 == 0 && aligned(y, 16) && aligned(codes, 4)) {
     const int64_t n_units = n / 8;
     const int grid = grid_for(c, n_units, kThreads * kUnroll);
     const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
     ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
       if (asym)
-        group_dequant_fast<OT, true, LL, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        group_dequant_fast<OT, true, LL, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
             codes32, scales, offsets, n_units, y), note_launches(1);
       else
-        group_dequant_fast<OT, false, LL, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        group_dequant_fast<OT, false, LL, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            codes32, scales, nullptr, n_units, y), note_launches(1);
+    }));
+    return 0;
+  }
+  L = pc ? 0 : lanes_for_group(g, 16);
+  if (L > 0 && n % 16 == 0 && aligned(y, 16) && aligned(codes, 8)) {
+    const int64_t n_units = n / 16;
+    const int grid = grid_for(c, n_units, kThreads * kUnroll);
+    const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
+    ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
+      if (asym)
+        group_dequant_fast<OT, true, LL, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+            codes32, scales, offsets, n_units, y), note_launches(1);
+      else
+        group_dequant_fast<OT, false, LL, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
             codes32, scales, nullptr, n_units, y), note_launches(1);
     }));
     return 0;

@@ -42,8 +42,8 @@ struct Workspace {
   double *partial;       // kMaxRowBlocks * cols per-CTA column partials
   uint32_t *counters;    // n_strips + 4 arrival counters / flags
   int n_strips;
-  int64_t *node_lo;      // pairwise-tree nodes
-  int64_t *node_n;
+  int32_t *node_lo;      // pairwise-tree nodes (used when cols > 16384)
+  int32_t *node_n;
   int32_t *node_left;
   double *node_val;
   size_t bytes;
@@ -63,6 +63,15 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot);
+
+// TMA-fed streaming variant of the fast group compress (stream.cu); L = lanes
+// per group at 8 elements per lane.
+int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                              int L, bool asym, const uint8_t *zero_flag, const int32_t *rank,
+                              uint16_t *outl_val, int64_t k_cap, uint8_t *codes, uint16_t *scales,
+                              uint16_t *offsets, uint32_t *err);
+// Tuning switch read once from the environment: ADC_COMPRESS_PATH=tma|regs (default regs).
+bool use_tma_compress();
 
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,

@@ -7,9 +7,10 @@
 //
 // One launch, three stages, chained with the last-block-done pattern (no grid
 // barrier, no cooperative launch, no global atomics on data):
-//   A. every CTA reduces a (rows/gy) x 256-column tile into per-CTA column
-//      partials, written to the workspace;
-//   B. the last CTA to finish in a column strip sums that strip's partials;
+//   A. every CTA reduces a (rows/gy) x 256-column tile into column partials;
+//      the 8 CTAs of a thread-block cluster (stacked along rows) combine
+//      theirs through distributed shared memory and write one partial;
+//   B. the last cluster to finish in a column strip sums that strip's partials;
 //   C. the last strip to finish computes mean / std / z / flags / ranks.
 // Counters are reset by the CTAs that consume them, so the workspace stays
 // zero-filled between calls (it must be zero-filled once by the caller).
@@ -22,20 +23,31 @@
 // initial 0.0; restated in oracle/codec_oracle.py:pairwise_sum and pinned
 // against ndarray.sum), evaluated level-parallel here; every float64 op is an
 // explicit _rn intrinsic so nothing is contracted into an FMA.
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "launch.h"
 
+namespace cg = cooperative_groups;
+
 namespace adc {
+
+constexpr int kClusterY = 8;  // CTAs per cluster, stacked along rows
 
 constexpr double kExactLimit = 536870912.0;  // 2^29
 constexpr int kStripCols = 256;              // 32 column units of 8 per CTA
 
-// |f16| -> f64 without the conversion pipe: f16 -> f32 (HADD2.F32), then
-// re-bias the f32 exponent into an f64 (every f16 value is a normal f32).
-__device__ __forceinline__ double absh_to_f64(uint32_t bits) {
-  const uint32_t u = __float_as_uint(h2f(bits & 0x7fffu));
-  const uint32_t hi = u ? (u >> 3) + (896u << 20) : 0u;
-  return __hiloint2double(static_cast<int>(hi), static_cast<int>(u << 29));
+// f16 half of a packed word -> f64 in one F2F.F64.F16 (reads .H0/.H1 directly;
+// keeps the integer pipe free -- the bit-trick version was ALU-bound).
+__device__ __forceinline__ double h_lo_f64(uint32_t w) {
+  double r;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(static_cast<unsigned short>(w & 0xffffu)));
+  return r;
+}
+__device__ __forceinline__ double h_hi_f64(uint32_t w) {
+  double r;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(static_cast<unsigned short>(w >> 16)));
+  return r;
 }
 
 // ---------------------------------------------------------------------------
@@ -73,50 +85,51 @@ struct Term {  // element i of the summed vector: S[i] or (S[i]-mean)^2
   const double *s;
   double mean;
   bool squared;
-  __device__ __forceinline__ double operator()(int64_t i) const {
-    const double v = __ldcg(s + i);
+  __device__ __forceinline__ double map(double v) const {
     if (!squared) return v;
     const double d = __dsub_rn(v, mean);
     return __dmul_rn(d, d);
   }
 };
 
-// One leaf of pairwise_sum_DOUBLE computed by an aligned group of 8 lanes:
-// lane j owns accumulator r[j]; the final ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7))
-// is built with width-8 shuffles in exactly that order; lane 0 adds the
-// n % 8 remainder sequentially.  All 32 lanes must call it.
-__device__ __forceinline__ double leaf_sum8(const Term &t, int64_t lo, int64_t n, bool valid) {
+// One leaf (n <= 128) of pairwise_sum_DOUBLE computed by an aligned group of
+// 8 lanes: lane j owns accumulator r[j] = a[j] + a[j+8] + ... (in order); the
+// final ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) is built with width-8 shuffles in
+// exactly that order; lane 0 adds the n % 8 remainder sequentially.  The 16
+// loads of a lane are issued together (one L2 round trip).  All 32 lanes call.
+__device__ __forceinline__ double leaf_sum8(const Term &t, int lo, int n, bool valid) {
   const int j = threadIdx.x & 7;
+  const int stop = n - (n % 8);
+  double v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (valid && 8 * i + j < stop) ? __ldcg(t.s + lo + 8 * i + j) : 0.0;
   double res = 0.0;
   if (valid && n >= 8) {
-    double r = t(lo + j);
-    const int64_t stop = n - (n % 8);
-    for (int64_t i = 8; i < stop; i += 8) r = __dadd_rn(r, t(lo + i + j));
+    double r = t.map(v[0]);
+#pragma unroll
+    for (int i = 1; i < 16; ++i)
+      if (8 * i < stop) r = __dadd_rn(r, t.map(v[i]));
     res = r;
   }
   const double a = __dadd_rn(res, __shfl_down_sync(0xffffffffu, res, 1, 8));
   const double b = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, 2, 8));
   double c = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, 4, 8));
   if (valid && j == 0) {
-    if (n < 8) {
-      c = 0.0;
-      for (int64_t i = 0; i < n; ++i) c = __dadd_rn(c, t(lo + i));
-    } else {
-      for (int64_t i = n - (n % 8); i < n; ++i) c = __dadd_rn(c, t(lo + i));
-    }
+    if (n < 8) c = 0.0;
+    for (int i = stop; i < n; ++i) c = __dadd_rn(c, t.map(__ldcg(t.s + lo + i)));
   }
   return c;
 }
 
 // Level-parallel evaluation of numpy's pairwise recursion over n values.
-// nodes: lo/n/left/val arrays in the workspace; s_lvl: level offsets (smem).
+// Node arrays live in shared memory when they fit, else in the workspace.
 struct Tree {
-  int64_t *lo, *n;
-  int32_t *left;
+  int32_t *lo, *n, *left;
   double *val;
 };
+constexpr int kSmemNodes = 1024;  // enough for n <= 16384 (leaves hold >= 56 values)
 
-__device__ int build_tree(int64_t n, const Tree &tr, int *s_lvl, int *s_tmp) {
+__device__ int build_tree(int n, const Tree &tr, int *s_lvl, int *s_tmp) {
   if (threadIdx.x == 0) {
     tr.lo[0] = 0;
     tr.n[0] = n;
@@ -131,15 +144,15 @@ __device__ int build_tree(int64_t n, const Tree &tr, int *s_lvl, int *s_tmp) {
     int next = e;
     for (int base = b; base < e; base += blockDim.x) {
       const int i = base + threadIdx.x;
-      const int64_t m = i < e ? tr.n[i] : 0;
+      const int m = i < e ? tr.n[i] : 0;
       const int internal = (i < e && m > 128) ? 1 : 0;
       int total;
       const int before = block_excl_scan(internal, &total, s_tmp);
       if (i < e) {
         if (internal) {
           const int l = next + 2 * before;
-          const int64_t lo = tr.lo[i];
-          int64_t h = m / 2;
+          const int lo = tr.lo[i];
+          int h = m / 2;
           h -= h % 8;
           tr.left[i] = l;
           tr.lo[l] = lo;
@@ -176,52 +189,79 @@ __device__ double tree_sum(const Term &t, const Tree &tr, int depth, const int *
     }
     __syncthreads();
   }
-  return __dadd_rn(0.0, tr.val[0]);
+  const double r = __dadd_rn(0.0, tr.val[0]);
+  __syncthreads();
+  return r;
 }
 
 // Stage C: mean / std / z-score flags / ranks / indices (codec.py:294-305, 324-341).
+// `scratch` is >= kStatsScratch bytes of shared memory (the stage-A buffers,
+// no longer live): tree nodes + a flag byte per column when cols <= 16384.
+constexpr int kStatsScratch = kSmemNodes * 20 + 16384;
 __device__ void outlier_stats_block(const double *S, int64_t rows, int64_t cols, double thr,
-                                    int64_t k_cap, const Tree &tr, uint8_t *flag, int32_t *rank,
-                                    uint32_t *idx, int32_t *k_out, uint32_t *err,
-                                    bool too_many_check) {
+                                    int64_t k_cap, const Tree &tr_global, uint8_t *flag,
+                                    int32_t *rank, uint32_t *idx, int32_t *k_out, uint32_t *err,
+                                    bool too_many_check, unsigned char *scratch) {
   __shared__ int s_lvl[72];
   __shared__ int s_tmp[32];
-  __shared__ int s_bad;
-  if (threadIdx.x == 0) s_bad = 0;
-  __syncthreads();
-  const double cap = 65504.0 * static_cast<double>(rows);
-  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
-    if (!(__ldcg(S + c) <= cap)) s_bad = 1;  // inf/NaN input (no finite f16 matrix reaches it)
-  const int depth = build_tree(cols, tr, s_lvl, s_tmp);
+  const bool small = cols <= 16384;
+  const Tree tr = small ? Tree{reinterpret_cast<int32_t *>(scratch),
+                               reinterpret_cast<int32_t *>(scratch + 4 * kSmemNodes),
+                               reinterpret_cast<int32_t *>(scratch + 8 * kSmemNodes),
+                               reinterpret_cast<double *>(scratch + 12 * kSmemNodes)}
+                        : tr_global;
+  uint8_t *sflag = small ? scratch + 20 * kSmemNodes : flag;
+  const int depth = build_tree(static_cast<int>(cols), tr, s_lvl, s_tmp);
   Term t{S, 0.0, false};
   const double mean = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
-  __syncthreads();
   t.mean = mean;
   t.squared = true;
   const double var = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
   const double sigma = __dsqrt_rn(var);
-  int64_t pos = 0;
-  for (int64_t base = 0; base < cols; base += blockDim.x) {
-    const int64_t c = base + threadIdx.x;
-    int f = 0;
-    if (c < cols && sigma != 0.0)
-      f = __ddiv_rn(__dsub_rn(__ldcg(S + c), mean), sigma) > thr ? 1 : 0;
-    int total;
-    const int before = block_excl_scan(f, &total, s_tmp);
-    if (c < cols) {
-      flag[c] = static_cast<uint8_t>(f);
-      const int64_t r = pos + before;
-      rank[c] = f ? static_cast<int32_t>(r) : -1;
-      if (f && r < k_cap) idx[r] = static_cast<uint32_t>(c);
+  // pass 1, coalesced and batched: z-score flags (strict >, codec.py:305)
+  const double cap = 65504.0 * static_cast<double>(rows);
+  int bad = 0;
+  for (int64_t base = 0; base < cols; base += 8 * static_cast<int64_t>(blockDim.x)) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t c = base + q * blockDim.x + threadIdx.x;
+      v[q] = c < cols ? __ldcg(S + c) : 0.0;
     }
-    pos += total;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int64_t c = base + q * blockDim.x + threadIdx.x;
+      if (c < cols) {
+        bad |= !(v[q] <= cap);  // inf/NaN input: no finite f16 matrix reaches this sum
+        const bool f = sigma != 0.0 && __ddiv_rn(__dsub_rn(v[q], mean), sigma) > thr;
+        sflag[c] = f ? 1 : 0;
+        if (small) flag[c] = f ? 1 : 0;
+      }
+    }
+  }
+  bad = __syncthreads_or(bad);
+  // pass 2: contiguous runs -> one block scan -> ranks and ascending indices
+  const int64_t run = (cols + blockDim.x - 1) / blockDim.x;
+  const int64_t c0 = min(cols, run * threadIdx.x), c1 = min(cols, c0 + run);
+  int mine = 0;
+  for (int64_t c = c0; c < c1; ++c) mine += sflag[c];
+  int total;
+  int pos = block_excl_scan(mine, &total, s_tmp);
+  for (int64_t c = c0; c < c1; ++c) {
+    if (sflag[c]) {
+      rank[c] = pos;
+      if (pos < k_cap) idx[pos] = static_cast<uint32_t>(c);
+      ++pos;
+    } else {
+      rank[c] = -1;
+    }
   }
   if (threadIdx.x == 0) {
-    *k_out = static_cast<int32_t>(pos);
+    *k_out = total;
     if (err) {
-      if (s_bad) atomicOr(err, ADC_ERR_NONFINITE);
-      if (too_many_check && 2 * pos > cols) atomicOr(err, ADC_ERR_TOO_MANY_OUTLIERS);
-      if (pos > k_cap) atomicOr(err, ADC_ERR_K_CAP);
+      if (bad) atomicOr(err, ADC_ERR_NONFINITE);
+      if (too_many_check && 2 * static_cast<int64_t>(total) > cols) atomicOr(err, ADC_ERR_TOO_MANY_OUTLIERS);
+      if (total > k_cap) atomicOr(err, ADC_ERR_K_CAP);
     }
   }
 }
@@ -249,8 +289,12 @@ struct ColArgs {
 };
 
 template <int DT, bool SUM>
-__global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x, ColArgs a) {
-  __shared__ double red[8][32][8];
+__global__ void __cluster_dims__(1, kClusterY, 1) __launch_bounds__(kThreads, 3)
+    colstats(const void *__restrict__ x, ColArgs a) {
+  // stage A/B buffers and the stage-C scratch share one allocation
+  __shared__ __align__(16) unsigned char s_raw[kStatsScratch > 18432 ? kStatsScratch : 18432];
+  double(*red)[32][8] = reinterpret_cast<double(*)[32][8]>(s_raw);
+  double *cpart = reinterpret_cast<double *>(s_raw + 16384);
   __shared__ int s_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t cols = a.cols, rows = a.rows;
@@ -264,17 +308,19 @@ __global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x,
   if (live) {
     const int64_t step = static_cast<int64_t>(gy) * 8;
     int64_t r = static_cast<int64_t>(blockIdx.y) * 8 + ty;
-    for (; r + 3 * step < rows; r += 4 * step) {
-      uint4 h[4];
+    for (; r + 7 * step < rows; r += 8 * step) {
+      uint4 h[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) h[q] = Loader<DT>::template load8<true>(x, (r + q * step) * cols + cu * 8);
+      for (int q = 0; q < 8; ++q) h[q] = Loader<DT>::template load8<true>(x, (r + q * step) * cols + cu * 8);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const uint32_t w[4] = {h[q].x, h[q].y, h[q].z, h[q].w};
         if (SUM) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            acc[j] = __dadd_rn(acc[j], absh_to_f64((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu));
+          for (int j = 0; j < 4; ++j) {
+            acc[2 * j] = __dadd_rn(acc[2 * j], fabs(h_lo_f64(w[j])));
+            acc[2 * j + 1] = __dadd_rn(acc[2 * j + 1], fabs(h_hi_f64(w[j])));
+          }
         } else {
 #pragma unroll
           for (int j = 0; j < 4; ++j) mx[j] = __vmaxu2(mx[j], w[j] & 0x7fff7fffu);
@@ -286,8 +332,10 @@ __global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x,
       const uint32_t w[4] = {h.x, h.y, h.z, h.w};
       if (SUM) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          acc[j] = __dadd_rn(acc[j], absh_to_f64((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu));
+        for (int j = 0; j < 4; ++j) {
+          acc[2 * j] = __dadd_rn(acc[2 * j], fabs(h_lo_f64(w[j])));
+          acc[2 * j + 1] = __dadd_rn(acc[2 * j + 1], fabs(h_hi_f64(w[j])));
+        }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; ++j) mx[j] = __vmaxu2(mx[j], w[j] & 0x7fff7fffu);
@@ -303,49 +351,71 @@ __global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x,
     for (int j = 0; j < 4; ++j) redu[(ty * 32 + tx) * 4 + j] = mx[j];
   }
   __syncthreads();
-  if (ty == 0 && live) {
+  // block partial of strip column t = 8*tx + j: reduce the 8 row lanes
+  {
+    const int t = threadIdx.x, ctx = t >> 3, cj = t & 7;
     if (SUM) {
-      double v[8];
+      double v = red[0][ctx][cj];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        v[j] = red[0][tx][j];
-#pragma unroll
-        for (int t = 1; t < 8; ++t) v[j] = __dadd_rn(v[j], red[t][tx][j]);
-      }
-      double *dst = a.partial + static_cast<int64_t>(blockIdx.y) * cols + cu * 8;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) __stcg(dst + j, v[j]);
+      for (int q = 1; q < 8; ++q) v = __dadd_rn(v, red[q][ctx][cj]);
+      cpart[t] = v;
     } else {
       const uint32_t *redu = reinterpret_cast<const uint32_t *>(&red[0][0][0]);
-      uint32_t *dst = reinterpret_cast<uint32_t *>(a.partial) + static_cast<int64_t>(blockIdx.y) * cols + cu * 8;
+      uint32_t v = 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        uint32_t v = redu[tx * 4 + j];
-#pragma unroll
-        for (int t = 1; t < 8; ++t) v = __vmaxu2(v, redu[(t * 32 + tx) * 4 + j]);
-        __stcg(dst + 2 * j, v & 0xffffu);
-        __stcg(dst + 2 * j + 1, v >> 16);
-      }
+      for (int q = 0; q < 8; ++q) v = max(v, (redu[(q * 32 + ctx) * 4 + (cj >> 1)] >> (16 * (cj & 1))) & 0xffffu);
+      reinterpret_cast<uint32_t *>(cpart)[t] = v;
     }
   }
-  // ---- stage B: the last CTA of this column strip reduces the strip
+  // cluster reduction over the kClusterY CTAs stacked along rows (DSMEM)
+  cg::cluster_group cluster = cg::this_cluster();
+  cluster.sync();
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * kStripCols + threadIdx.x;
+  const int64_t crow = blockIdx.y / kClusterY;
+  if (cluster.block_rank() == 0 && c < cols) {
+    if (SUM) {
+      double v[kClusterY];
+#pragma unroll
+      for (int r = 0; r < kClusterY; ++r) v[r] = *cluster.map_shared_rank(cpart + threadIdx.x, r);
+      double sum = v[0];
+#pragma unroll
+      for (int r = 1; r < kClusterY; ++r) sum = __dadd_rn(sum, v[r]);
+      __stcg(a.partial + crow * cols + c, sum);
+    } else {
+      uint32_t *cpu = reinterpret_cast<uint32_t *>(cpart);
+      uint32_t m = 0;
+#pragma unroll
+      for (int r = 0; r < kClusterY; ++r) m = max(m, *cluster.map_shared_rank(cpu + threadIdx.x, r));
+      __stcg(reinterpret_cast<uint32_t *>(a.partial) + crow * cols + c, m);
+    }
+  }
+  cluster.sync();  // peers' shared memory must outlive rank 0's reads
+  if (cluster.block_rank() != 0) return;
+  // ---- stage B: the last cluster of this column strip reduces the strip
+  const int gyc = gy / kClusterY;
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(a.strip_cnt + blockIdx.x, 1u) == static_cast<uint32_t>(gy - 1);
+  if (threadIdx.x == 0) s_last = atomicAdd(a.strip_cnt + blockIdx.x, 1u) == static_cast<uint32_t>(gyc - 1);
   __syncthreads();
   if (!s_last) return;
   __threadfence();
-  const int64_t c = static_cast<int64_t>(blockIdx.x) * kStripCols + threadIdx.x;
   if (c < cols) {
     if (SUM) {
-      double s = 0.0;
-      for (int b = 0; b < gy; ++b) s = __dadd_rn(s, __ldcg(a.partial + static_cast<int64_t>(b) * cols + c));
+      double p4[4] = {0.0, 0.0, 0.0, 0.0};
+      int b = 0;
+      for (; b + 4 <= gyc; b += 4) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          p4[q] = __dadd_rn(p4[q], __ldcg(a.partial + static_cast<int64_t>(b + q) * cols + c));
+      }
+      for (; b < gyc; ++b) p4[0] = __dadd_rn(p4[0], __ldcg(a.partial + static_cast<int64_t>(b) * cols + c));
+      const double s = __dadd_rn(__dadd_rn(p4[0], p4[1]), __dadd_rn(p4[2], p4[3]));
       __stcg(a.S + c, s);
       if (!(s < kExactLimit)) atomicOr(a.done_cnt + 1, 1u);
     } else {
       const uint32_t *p = reinterpret_cast<const uint32_t *>(a.partial);
       uint32_t m = 0;
-      for (int b = 0; b < gy; ++b) m = max(m, __ldcg(p + static_cast<int64_t>(b) * cols + c));
+      for (int b = 0; b < gyc; ++b) m = max(m, __ldcg(p + static_cast<int64_t>(b) * cols + c));
       __stcg(a.colmax + c, m);
       if (m >= 0x7c00u && a.err) atomicOr(a.err, ADC_ERR_NONFINITE);
     }
@@ -374,7 +444,7 @@ __global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x,
   __syncthreads();
   if (a.do_stats)
     outlier_stats_block(a.S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.rank, a.idx, a.k_out,
-                        a.err, a.too_many_check != 0);
+                        a.err, a.too_many_check != 0, s_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -383,6 +453,7 @@ __global__ void __launch_bounds__(kThreads) colstats(const void *__restrict__ x,
 // ---------------------------------------------------------------------------
 template <int DT, bool SUM>
 __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restrict__ x, ColArgs a) {
+  __shared__ __align__(16) unsigned char s_raw[kStatsScratch];
   __shared__ int s_last;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; c < a.cols;
        c += static_cast<int64_t>(gridDim.x) * kThreads) {
@@ -409,7 +480,7 @@ __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restr
   __syncthreads();
   if (a.do_stats)
     outlier_stats_block(a.S, a.rows, a.cols, a.thr, a.k_cap, a.tree, a.flag, a.rank, a.idx,
-                        a.k_out, a.err, a.too_many_check != 0);
+                        a.k_out, a.err, a.too_many_check != 0, s_raw);
 }
 
 // ---------------------------------------------------------------------------
@@ -442,11 +513,15 @@ static bool fast_cols(const void *x, int64_t cols) {
 
 static dim3 col_grid(const Ctx &c, int64_t rows, int64_t cols) {
   dim3 g(static_cast<unsigned>((cols + kStripCols - 1) / kStripCols), 1);
-  int64_t want = (static_cast<int64_t>(c.num_sms) * 4 + g.x - 1) / g.x;
+  // many short CTAs (measured: gy = 128 beats one wave of long CTAs: the
+  // tail of a partial second wave costs more than the extra partials)
+  (void)c;
+  int64_t want = kMaxRowBlocks;
   const int64_t maxy = (rows + 7) / 8;
   if (want > kMaxRowBlocks) want = kMaxRowBlocks;
   if (want > maxy) want = maxy;
-  g.y = static_cast<unsigned>(want < 1 ? 1 : want);
+  want = (want + kClusterY - 1) / kClusterY * kClusterY;  // whole clusters
+  g.y = static_cast<unsigned>(want < kClusterY ? kClusterY : want);
   return g;
 }
 

@@ -218,8 +218,14 @@ def normalized(scales, offsets, codes, idx, vals, mask_bits):
 
     idx = None if idx is None or len(idx) == 0 else np.asarray(idx, np.uint32)
     vals = None if idx is None else f16bits(vals)
+    off = f16bits(offsets)
+    if off is not None:
+        # An all-zero group's offset is (hi+lo)/2 of zeros; its SIGN is whatever
+        # numpy's SIMD max/min returns for a tie between -0.0 and +0.0 (CPU
+        # dependent).  Numerically identical; compared as +0.
+        off = np.where(off == 0x8000, np.uint16(0), off).astype(np.uint16)
     return {
-        "scales": f16bits(scales), "offsets": f16bits(offsets), "codes": u8(codes),
+        "scales": f16bits(scales), "offsets": off, "codes": u8(codes),
         "idx": idx, "vals": vals, "mask": u8(mask_bits),
     }
 

@@ -214,3 +214,46 @@ def test_wire_format_matches_oracle_bytes(torch_cuda, spec_args):
     back = adc.deserialize(blob)
     assert adc.serialize(back) == blob
     assert np.array_equal(adc.decompress(back).cpu().numpy(), adc.decompress(ct).cpu().numpy())
+
+
+def _bf16_adversarial(rng, rows=256, cols=512):
+    """bf16-representable values that stress the native bf16 path."""
+    import torch
+    x = rng.normal(size=(rows, cols)).astype(np.float32)
+    x[:, 0:8] *= 1e-6          # tiny values needing f16 subnormal rounding
+    x[:, 8:16] = rng.choice([0.0, 2 ** -20, -(2 ** -18), 3 * 2 ** -22], size=(rows, 8))
+    x[0:4, :] *= 1e-7          # whole tiny groups (row-major groups of 128)
+    x[4:8, :] = np.round(x[4:8, :] * 8) / 8   # exact ties for power-of-two scales
+    x[8:12, 100:110] = 65280.0                # largest finite-after-cast bf16
+    return torch.from_numpy(x).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("scheme,group", [(0, 128), (0, 16), (0, 256), (1, 128), (1, 16), (2, 128), (0, 0)])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_bf16_native_path_adversarial(torch_cuda, scheme, group, seed):
+    torch = torch_cuda
+    xt = _bf16_adversarial(np.random.default_rng(seed))
+    want = oracle_run(xt.to(torch.float32).numpy(), scheme, group, 3.0)
+    got = device_run(xt, scheme, group, 3.0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
+
+
+def test_bf16_asym_tie_families(torch_cuda):
+    """The Appendix A.5 tie families are bf16-exact: run them natively in bf16."""
+    torch = torch_cuda
+    for name, x, s, g, t in cases.tie_family_cases():
+        xt = torch.from_numpy(x).to(torch.bfloat16)
+        want = oracle_run(xt.to(torch.float32).numpy(), s, g, t)
+        got = device_run(xt, s, g, t)
+        assert cases.norm_digest(*got) == cases.norm_digest(*want), name
+
+
+def test_bf16_overflow_is_nonfinite(torch_cuda):
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    x = torch.ones(4, 256, dtype=torch.bfloat16)
+    x[2, 7] = 65536.0  # rounds to f16 inf (codec.py:167-170)
+    for spec in (adc.SchemeSpec(adc.Scheme.SYMMETRIC_GROUP), adc.SchemeSpec(adc.Scheme.ASYMMETRIC_GROUP),
+                 adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), adc.SchemeSpec(adc.Scheme.SYMMETRIC_GROUP, 0)):
+        with pytest.raises(adc.NonFiniteInputError):
+            adc.compress(x, spec)
