@@ -130,6 +130,43 @@ __device__ __forceinline__ void unit_codes_exact(const uint32_t *w, float s, flo
   }
 }
 
+// Exact asymmetric code of one element (h = its f16 value) for the elements
+// whose fast quotient fell within the tie margin -- frequent for bf16 data,
+// whose few mantissa bits make exact half-integer quotients common.
+//   d = h - o with its TwoSum error (non-zero: a tiny element against a
+//   large offset -> float64, as codec.py:223-231);
+//   r = Markstein-refined d/s; within 2^-20 of a half-integer b the exact
+//   residual d - b*s (one FMA, exact here) decides, ties to even.
+__device__ __noinline__ int asym_exact_code(float h, float s, float inv, float o) {
+  const float d = h - o;
+  const float bb = d - h;
+  const float err = (h - (d - bb)) + (-o - bb);
+  if (err != 0.f) {
+    const double r = rint((static_cast<double>(h) - static_cast<double>(o)) / static_cast<double>(s));
+    return static_cast<int>(fmin(fmax(r, -8.0), 7.0));
+  }
+  const float r0 = d * inv;
+  const float r1 = fmaf(fmaf(-r0, s, d), inv, r0);
+  const float c = (r1 + kMagic) - kMagic;  // RNE integer
+  const float fr = r1 - c;
+  int code = static_cast<int>(c);
+  if (fabsf(fabsf(fr) - 0.5f) < 0x1p-20f) {
+    const float bnd = c + (fr > 0.f ? 0.5f : -0.5f);  // nearest half-integer
+    const float res = fmaf(-bnd, s, d);               // exact sign of q - bnd
+    const float up = bnd + 0.5f, dn = bnd - 0.5f;
+    const float even = (fmodf(up, 2.f) == 0.f) ? up : dn;
+    code = static_cast<int>(res > 0.f ? up : (res < 0.f ? dn : even));
+  }
+  return min(max(code, -8), 7);
+}
+
+// f16 value (as float) of element i of the input, re-read from global memory
+// (the rare exact path only).
+template <int DT>
+__device__ __forceinline__ float elem_f16(const void *x, int64_t i) {
+  return h2f(Loader<DT>::load1(x, i));
+}
+
 // Fast group kernel: a lane owns EPL (8 or 16) consecutive elements, a group
 // of g = EPL*L elements is owned by L adjacent lanes; U units per lane are
 // loaded before any is processed (memory-level parallelism).
@@ -226,14 +263,14 @@ __global__ void __launch_bounds__(kThreads, 4)
       }
       if (!act) continue;
       uint32_t t[EPL];
+      uint32_t fix = 0;  // elements whose fast quotient is within the tie margin
       if (ASYM) {
         const QParams q = make_qparams(s_bits, o_bits);
         // r is within 2^-18.8 of the exact quotient of the f16 value; for bf16
         // the native x differs from f16(x) by <= 2^-25 (tiny values only), i.e.
-        // by <= 2^-25/s in the quotient.  Units with any r inside that margin
-        // of a half-integer are redone exactly (branch per unit, not element).
-        const float margin = 0x1p-17f + (BF ? 0x1p-25f * q.inv : 0.f);
-        float worst = 0.f;
+        // by <= 2^-25/s in the quotient.  Elements inside that margin of a
+        // half-integer are redone exactly after packing.
+        const float thr = 0.5f - (0x1p-17f + (BF ? 0x1p-25f * q.inv : 0.f));
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
 #pragma unroll
@@ -241,11 +278,10 @@ __global__ void __launch_bounds__(kThreads, 4)
             const float xv = hh ? R::hi(w[k][i]) : R::lo(w[k][i]);
             const float r = fminf(fmaxf((xv - q.o) * q.inv, -8.f), 7.f);
             const float tv = r + kMagic8;
-            worst = fmaxf(worst, fabsf(r - (tv - kMagic8)));
+            fix |= (fabsf(r - (tv - kMagic8)) > thr ? 1u : 0u) << (2 * i + hh);
             t[2 * i + hh] = __float_as_uint(tv);
           }
         }
-        if (worst > 0.5f - margin) unit_codes_exact<BF, NW>(w[k], h2f(s_bits), q.o, true, t);
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
           const float sc = h2f(s_bits), inv = rcp_approx(sc);
@@ -265,10 +301,25 @@ __global__ void __launch_bounds__(kThreads, 4)
       } else {  // bf16 group with a tiny maximum: exact converting path
         unit_codes_exact<BF, NW>(w[k], h2f(s_bits), 0.f, false, t);
       }
+      uint32_t c0 = pack8_tbits(t), c1 = NC == 2 ? pack8_tbits(t + 8) : 0u;
+      if (ASYM) {
+        const float sc = h2f(s_bits), so = h2f(o_bits);
+        const float scd = sc == 0.f ? 1.f : sc, inv = rcp_approx(scd);
+        while (fix) {  // per-lane, proportional to the number of near-ties
+          const int i = __ffs(fix) - 1;
+          fix &= fix - 1;
+          const int code = asym_exact_code(elem_f16<DT>(x, u * EPL + i), scd, inv, so);
+          const uint32_t sh = 4 * (i & 7), nib = static_cast<uint32_t>(code) & 0xfu;
+          if (i < 8)
+            c0 = (c0 & ~(0xfu << sh)) | (nib << sh);
+          else
+            c1 = (c1 & ~(0xfu << sh)) | (nib << sh);
+        }
+      }
       if (NC == 1) {
-        codes[u] = pack8_tbits(t);
+        codes[u] = c0;
       } else {
-        *reinterpret_cast<uint2 *>(codes + 2 * u) = make_uint2(pack8_tbits(t), pack8_tbits(t + 8));
+        *reinterpret_cast<uint2 *>(codes + 2 * u) = make_uint2(c0, c1);
       }
     }
   }
