@@ -258,11 +258,17 @@ def compress_async(x: torch.Tensor, spec: SchemeSpec, *, k_cap: int | None = Non
     scales = torch.empty(n_groups, dtype=torch.float16, device=dev)
     offsets = (torch.empty(n_groups, dtype=torch.float16, device=dev)
                if scheme is Scheme.ASYMMETRIC_GROUP else None)
+    shared = status is not None
     if status is None:
         status = torch.zeros(2, dtype=torch.int32, device=dev)
     idx = val = None
     kc = 0
+    kbuf = status
     if scheme is Scheme.OUTLIER_SEPARATED:
+        # k is per tensor (the decompress scatter reads it); only the error
+        # word may be shared between calls
+        if shared:
+            kbuf = torch.zeros(2, dtype=torch.int32, device=dev)
         kc = cols // 2 if k_cap is None else int(k_cap)
         idx = torch.empty(max(kc, 1), dtype=torch.int32, device=dev)
         val = torch.empty((max(kc, 1), rows), dtype=torch.float16, device=dev)
@@ -274,16 +280,17 @@ def compress_async(x: torch.Tensor, spec: SchemeSpec, *, k_cap: int | None = Non
     st = _lib.lib().adc_compress(
         int(scheme), x.data_ptr(), _DT[x.dtype], rows, cols, spec.group_size,
         float(spec.z_threshold), kc, codes.data_ptr(), scales.data_ptr(), _ptr(offsets),
-        _ptr(idx), _ptr(val), status.data_ptr() + 4 if idx is not None else None,
+        _ptr(idx), _ptr(val), kbuf.data_ptr() + 4 if idx is not None else None,
         status.data_ptr(), _ptr(ws), ws_bytes, _stream())
     _lib.check(st, "compress")
     return CompressedTensor(scheme, rows, cols, spec.group_size, scales, offsets, codes,
-                            outlier_indices=idx, outlier_values=val, k_dev=status, k_cap=kc,
+                            outlier_indices=idx, outlier_values=val, k_dev=kbuf, k_cap=kc,
                             shape=shape, dtype=dtype)
 
 
 def _finalize(ct: CompressedTensor) -> CompressedTensor:
-    """Parity mode: synchronise, raise reference errors, trim outliers to k."""
+    """Parity mode (private status = [error word, k]): synchronise, raise
+    reference errors, trim outliers to k."""
     err, k = (int(v) for v in ct.k_dev.cpu().tolist())
     err &= 0xffffffff
     raise_for_error_word(err, rows=ct.rows, cols=ct.cols, k=k)

@@ -35,9 +35,10 @@ __device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
 
 // Zero the flagged channels of 8 consecutive elements (one row segment,
 // codec.py:328-329) and copy their original f16 values into the (k, rows)
-// side buffer (codec.py:340).  The flag test is inline; the rare hit path is
-// out of line to keep registers.
-__device__ __noinline__ void zero_outlier_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
+// side buffer (codec.py:340).  Fully inlined with static indices so the
+// unit's words stay in registers (an out-of-line call forced them through
+// local memory on every unit); the hit branch is rare.
+__device__ __forceinline__ void zero_outlier_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
                                               const int32_t *__restrict__ rank,
                                               uint16_t *__restrict__ outl_val, int64_t rows,
                                               int64_t k_cap, bool bf16_words) {

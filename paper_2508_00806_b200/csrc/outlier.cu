@@ -250,7 +250,10 @@ __device__ void outlier_stats_block(const double *S, int64_t rows, int64_t cols,
   for (int64_t c = c0; c < c1; ++c) {
     if (sflag[c]) {
       rank[c] = pos;
-      if (pos < k_cap) idx[pos] = static_cast<uint32_t>(c);
+      if (pos < k_cap)
+        idx[pos] = static_cast<uint32_t>(c);
+      else
+        flag[c] = 0;  // beyond the side buffer: left in its groups (graceful overflow)
       ++pos;
     } else {
       rank[c] = -1;

@@ -50,7 +50,7 @@ __device__ __forceinline__ uint32_t fdiv_u32(uint32_t n, const FastDiv &f) {
 }
 
 // rare path of the outlier zeroing: copy + zero flagged lanes of one unit
-__device__ __noinline__ void stream_zero_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
+__device__ __forceinline__ void stream_zero_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
                                              const int32_t *__restrict__ rank,
                                              uint16_t *__restrict__ outl_val, int64_t rows,
                                              int64_t k_cap) {

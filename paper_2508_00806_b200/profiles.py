@@ -120,6 +120,10 @@ class ModelProfile:
         if self.reference_batch < 1 or self.n_layers < 1 or self.base_step_time_ms <= 0:
             raise ValidationError("n_layers, reference_batch and base_step_time_ms must be positive")
 
+    @property
+    def n_operators(self) -> int:
+        return len(self.operators)
+
     def to_dict(self) -> dict:
         return {
             "n_layers": self.n_layers, "static_mem_bytes": self.static_mem_bytes,

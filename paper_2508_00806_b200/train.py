@@ -1,0 +1,200 @@
+"""Adacc-policy GPT training on B200 (BASELINE configs[1] and [3]).
+
+    python -m paper_2508_00806_b200.train --model gpt-345m --batch 8 --steps 20 \
+        --policy adacc --mem-cap-gb 40
+    torchrun --nproc-per-node 8 -m paper_2508_00806_b200.train --model gpt-1.3b ...
+
+Flow (Fig. 5): profile one block on the device (profiler.py) ->
+plan with the exact planner under the HBM cap (policy.py; the reference's
+``planner.solve`` accepts the same JSON) -> train with the plan applied by
+saved-tensor hooks (hooks.py).  Data parallel over NCCL: the codec is
+rank-local and the only collective is DDP's bucketed gradient all-reduce.
+Synthetic learnable corpus (seeded Markov stream; no network for datasets).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import time
+
+import torch
+import torch.distributed as dist
+
+from . import policy as P
+from .gpt import BLOCK_OPS, GPT, GPTConfig, synthetic_batch
+from .hooks import COMPRESS, RECOMPUTE, RETAIN, ActivationPolicy
+from .profiler import profile_model
+from .profiles import save_profile
+
+STRATEGIES = ("retain-all", "full-recompute", "all-compress", "adacc")
+
+
+def plan_for(strategy: str, prof=None) -> dict:
+    ids = [o.op_id for o in BLOCK_OPS]
+    if strategy == "adacc":
+        return P.solve(prof).by_op(ids)
+    names = {P.RETAIN: RETAIN, P.COMPRESS: COMPRESS, P.RECOMPUTE: RECOMPUTE}
+    n = len(ids)
+    if strategy == "retain-all":
+        ch = (P.RETAIN,) * n
+    elif strategy == "all-compress":
+        ch = (P.COMPRESS,) * n
+    else:
+        ch = (P.RETAIN,) + (P.RECOMPUTE,) * (n - 1)
+    return {i: names[c] for i, c in zip(ids, ch)}
+
+
+class Trainer:
+    def __init__(self, cfg: GPTConfig, batch: int, *, lr: float = 3e-4, rank: int = 0,
+                 world: int = 1, device=None, ddp: bool = False):
+        self.cfg, self.batch, self.rank, self.world = cfg, batch, rank, world
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        torch.manual_seed(1234)
+        model = GPT(cfg).to(self.device, dtype=torch.bfloat16)
+        self.model = model
+        self.net = model
+        if ddp:
+            from torch.nn.parallel import DistributedDataParallel as DDP
+            self.net = DDP(model, device_ids=[self.device.index], gradient_as_bucket_view=True,
+                           bucket_cap_mb=64)
+        self.opt = torch.optim.AdamW(model.parameters(), lr=lr, betas=(0.9, 0.95), weight_decay=0.1,
+                                     fused=True)
+        self.pol = ActivationPolicy(BLOCK_OPS)
+        self.step_id = 0
+
+    def batch_at(self, step):
+        return synthetic_batch(step, self.rank, self.batch, self.cfg.seq, self.cfg.vocab, self.device)
+
+    def _forward(self, idx, tgt, pol):
+        # DDP wraps the module; our forward takes the policy as an argument
+        return self.net(idx, tgt, pol, self.step_id)
+
+    def step(self, idx, tgt) -> torch.Tensor:
+        loss = self._forward(idx, tgt, self.pol)
+        loss.backward()
+        self.opt.step()
+        self.opt.zero_grad(set_to_none=True)
+        self.step_id += 1
+        return loss.detach()
+
+    def static_bytes(self) -> int:
+        return torch.cuda.memory_allocated(self.device)
+
+    def profile(self, mem_budget_bytes: int, base_step_ms: float):
+        idx, tgt = self.batch_at(10**6)
+        prof, k_caps = profile_model(self.model, BLOCK_OPS, lambda: (idx, tgt),
+                                     mem_budget_bytes=mem_budget_bytes,
+                                     static_mem_bytes=self.static_after_step,
+                                     base_step_time_ms=base_step_ms, reference_batch=self.batch)
+        return prof, k_caps
+
+
+def _clone_state(sd):
+    if isinstance(sd, dict):
+        return {k: _clone_state(v) for k, v in sd.items()}
+    if isinstance(sd, list):
+        return [_clone_state(v) for v in sd]
+    if isinstance(sd, torch.Tensor):
+        return sd.detach().clone()
+    return sd
+
+
+def run(args) -> dict:
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = GPTConfig.named(args.model)
+    cfg.seq = args.seq or cfg.seq
+    tr = Trainer(cfg, args.batch, rank=rank, world=world, device=dev, ddp=world > 1)
+    total_hbm = torch.cuda.get_device_properties(dev).total_memory
+    cap = int(args.mem_cap_gb * (1 << 30)) if args.mem_cap_gb else total_hbm
+    # warm-up with retain-all to size static memory and the base step time
+    tr.pol.plan = plan_for("retain-all")
+    for s in range(2):
+        tr.step(*tr.batch_at(s))
+    torch.cuda.synchronize()
+    tr.static_after_step = torch.cuda.memory_allocated(dev)
+    t0 = time.perf_counter()
+    tr.step(*tr.batch_at(2))
+    torch.cuda.synchronize()
+    base_ms = (time.perf_counter() - t0) * 1e3
+    out = {"model": args.model, "params": tr.model.n_params(), "batch_per_gpu": args.batch,
+           "seq": cfg.seq, "n_gpus": world, "mem_cap_bytes": cap, "results": {}}
+    prof = None
+    if "adacc" in args.policy or args.profile_out:
+        prof, k_caps = tr.profile(cap, base_ms)
+        tr.pol.k_caps = k_caps
+        if args.profile_out and rank == 0:
+            save_profile(prof, args.profile_out)
+        out["profile"] = prof.to_dict()
+    losses_all = {}
+    # every strategy starts from the same weights / optimizer state and sees
+    # the same batches, so losses are comparable (retain vs recompute: equal)
+    snap_model = {k: v.detach().clone() for k, v in tr.model.state_dict().items()}
+    snap_opt = _clone_state(tr.opt.state_dict())
+    for strategy in args.policy.split(","):
+        plan = plan_for(strategy, prof)
+        tr.pol.plan = plan
+        tr.model.load_state_dict(snap_model)
+        tr.opt.load_state_dict(_clone_state(snap_opt))
+        tr.step_id = 0
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        for s in range(args.warmup):
+            tr.step(*tr.batch_at(100 + s))
+        batches = [tr.batch_at(1000 + s) for s in range(args.steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        losses = []
+        for idx, tgt in batches:
+            losses.append(tr.step(idx, tgt))
+        b.record()
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        tokens = args.batch * cfg.seq * world * args.steps
+        err = tr.pol.check()
+        peak = torch.cuda.max_memory_allocated(dev)
+        out["results"][strategy] = {
+            "plan": plan, "tokens_per_s": tokens / (ms / 1e3), "ms_per_step": ms / args.steps,
+            "peak_bytes": peak, "fits_cap": peak <= cap, "final_loss": float(losses[-1].item()),
+            "mean_loss": statistics.mean(float(l.item()) for l in losses), "device_error_word": err,
+            "compressed_tensors": tr.pol.stats.compressed, "recomputed_tensors": tr.pol.stats.recomputed,
+        }
+        losses_all[strategy] = [float(l.item()) for l in losses]
+    return out
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="gpt-345m")
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--seq", type=int, default=0)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--policy", default="retain-all,adacc")
+    ap.add_argument("--mem-cap-gb", type=float, default=0.0)
+    ap.add_argument("--profile-out", default="")
+    args = ap.parse_args(argv)
+    out = run(args)
+    if int(os.environ.get("RANK", "0")) == 0:
+        print(json.dumps(out))
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

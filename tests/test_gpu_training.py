@@ -1,0 +1,97 @@
+"""Adacc policies applied to a real GPT on the device (hooks, profiler, planner).
+
+Tolerances: RECOMPUTE must reproduce retain-all gradients exactly (same ops,
+same inputs); COMPRESS perturbs saved activations by at most scale/2 per
+element (tests/test_codec_properties.py:40-65), so gradients are compared by
+cosine similarity (>= 0.98) and the loss trajectory within 2% relative --
+looser than the paper's 0.5% end-of-training gap because these are 20-step
+runs on a tiny model.
+"""
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def tiny():
+    import torch
+    from paper_2508_00806_b200.gpt import GPTConfig
+    torch.cuda.init()
+    return GPTConfig(vocab=512, n_layer=2, n_head=4, d_model=256, seq=256, attn_dropout=0.1)
+
+
+def _grads(cfg, plan_name, seed=0):
+    import torch
+    from paper_2508_00806_b200.gpt import BLOCK_OPS, GPT, synthetic_batch
+    from paper_2508_00806_b200.hooks import ActivationPolicy
+    from paper_2508_00806_b200.train import plan_for
+    torch.manual_seed(seed)
+    model = GPT(cfg).cuda().to(torch.bfloat16)
+    pol = ActivationPolicy(BLOCK_OPS, plan_for(plan_name), min_numel=1024)
+    idx, tgt = synthetic_batch(0, 0, 4, cfg.seq, cfg.vocab, "cuda")
+    loss = model(idx, tgt, pol, seed=3)
+    loss.backward()
+    # embedding gradients are accumulated with atomics (order-nondeterministic
+    # even for retain-all): compare every other parameter
+    g = torch.cat([p.grad.float().flatten() for n, p in model.named_parameters()
+                   if not n.startswith(("wte", "wpe"))])
+    return loss.item(), g, pol
+
+
+def test_recompute_is_exact(tiny):
+    import torch
+    l0, g0, _ = _grads(tiny, "retain-all")
+    l1, g1, pol = _grads(tiny, "full-recompute")
+    assert pol.stats.recomputed > 0
+    assert l0 == l1
+    assert torch.equal(g0, g1)
+
+
+def test_compress_close(tiny):
+    import torch
+    l0, g0, _ = _grads(tiny, "retain-all")
+    l1, g1, pol = _grads(tiny, "all-compress")
+    assert pol.stats.compressed >= 8
+    assert pol.stats.stored_bytes < 0.45 * pol.stats.original_bytes
+    assert l0 == l1  # forward is unchanged by saving policies
+    cos = torch.nn.functional.cosine_similarity(g0, g1, dim=0).item()
+    assert cos > 0.98, cos
+    assert pol.check() == 0
+
+
+def test_profile_plan_train_loop(tiny, tmp_path):
+    import argparse
+    import json
+    from paper_2508_00806_b200 import train
+    from paper_2508_00806_b200.profiles import load_profile
+    args = argparse.Namespace(model="gpt-small-test", batch=8, seq=256, steps=30, warmup=2,
+                              policy="retain-all,full-recompute,all-compress,adacc",
+                              mem_cap_gb=0.0, profile_out=str(tmp_path / "prof.json"))
+    out = train.run(args)
+    prof = load_profile(tmp_path / "prof.json")
+    assert prof.n_operators == 11
+    assert all(op.compression_rate < 0.5 for op in prof.operators if op.kind.value != "dropout_mask" and op.mem_bytes > 1)
+    res = out["results"]
+    base = res["retain-all"]["final_loss"]
+    assert res["full-recompute"]["final_loss"] == base  # recompute is exact
+    for k in ("all-compress", "adacc"):
+        assert abs(res[k]["final_loss"] - base) / base < 0.02, (k, res[k]["final_loss"], base)
+    assert res["full-recompute"]["peak_bytes"] < res["retain-all"]["peak_bytes"]
+    assert res["all-compress"]["peak_bytes"] < res["retain-all"]["peak_bytes"]
+    json.dumps(out)
+
+
+def test_capped_plan_fits(tiny):
+    """Under a tight HBM cap the planner must pick memory-saving choices that fit."""
+    import argparse
+    from paper_2508_00806_b200 import train
+    args = argparse.Namespace(model="gpt-small-test", batch=8, seq=256, steps=3, warmup=1,
+                              policy="retain-all", mem_cap_gb=0.0, profile_out="")
+    free = train.run(args)["results"]["retain-all"]["peak_bytes"]
+    cap_gb = free * 0.75 / (1 << 30)
+    args.policy, args.mem_cap_gb = "adacc", cap_gb
+    out = train.run(args)
+    res = out["results"]["adacc"]
+    assert any(v != "retain" for v in res["plan"].values())
+    assert res["peak_bytes"] < free
