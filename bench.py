@@ -347,6 +347,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
     e2e_value = world * bytes_step * e2e_steps / (float(e_ms.item()) / 1e3) / 1e9
 
+    training = None
+    if not args.no_train:
+        training = run_training(args, world)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         procs = host_cores()
@@ -366,8 +369,31 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps},
                 "clocks": clocks.summary(), "gpu_launches": int(launches),
-                "device_error_word": status_err, "per_op": per_op}
+                "device_error_word": status_err, "per_op": per_op, "training": training}
         print(json.dumps(line), flush=True)
+
+
+def run_training(args, world):
+    """BASELINE configs[1]: GPT-345M training step, batch 8 x seq 1024 per GPU,
+    bf16, Adacc plan under an HBM cap (retain-all does not fit), DDP over NCCL
+    when N > 1.  Same weights and batches for every strategy."""
+    import argparse as _ap
+    from paper_2508_00806_b200 import train
+    targs = _ap.Namespace(model=args.train_model, batch=8, seq=0, steps=args.train_steps, warmup=3,
+                          policy="retain-all,full-recompute,all-compress,adacc",
+                          mem_cap_gb=args.train_cap_gb, profile_out="")
+    out = train.run(targs)
+    res = out["results"]
+    ad = res["adacc"]
+    return {"metric": "training tokens/s (Adacc plan, HBM cap)", "value": round(ad["tokens_per_s"], 1),
+            "unit": "tokens/s", "n_gpus": world, "model": out["model"], "params": out["params"],
+            "batch_per_gpu": out["batch_per_gpu"], "seq": out["seq"], "steps": args.train_steps,
+            "hbm_cap_bytes": out["mem_cap_bytes"], "scaling": "weak",
+            "plan": ad["plan"],
+            "strategies": {k: {"tokens_per_s": round(v["tokens_per_s"], 1), "ms_per_step": round(v["ms_per_step"], 2),
+                               "peak_bytes": v["peak_bytes"], "fits_cap": v["fits_cap"],
+                               "final_loss": round(v["final_loss"], 5)} for k, v in res.items()},
+            "profile": out.get("profile")}
 
 
 def main():
@@ -378,6 +404,11 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--no-train", action="store_true", help="skip the training tokens/s leg")
+    ap.add_argument("--train-model", default="gpt-345m")
+    ap.add_argument("--train-steps", type=int, default=10)
+    ap.add_argument("--train-cap-gb", type=float, default=20.0,
+                    help="HBM cap for the Adacc plan (retain-all needs ~30 GB at GPT-345M b8)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))

@@ -468,6 +468,22 @@ def detect_outlier_channels(x, threshold: float = DEFAULT_Z_THRESHOLD) -> torch.
     return idx[:k].to(torch.int64)
 
 
+def count_outliers_async(x: torch.Tensor, threshold: float = DEFAULT_Z_THRESHOLD) -> torch.Tensor:
+    """Launch outlier detection on a (rows, cols) CUDA tensor without
+    synchronising; returns the int32 device pair [error word, k].  Used at
+    policy-evolution tracking iterations (section 3.4)."""
+    rows, cols = x.shape
+    ws_bytes = _lib.lib().adc_workspace_bytes(int(Scheme.OUTLIER_SEPARATED), rows, cols, 0)
+    ws = torch.zeros(ws_bytes, dtype=torch.uint8, device=x.device)
+    idx = torch.empty(1, dtype=torch.int32, device=x.device)
+    status = torch.zeros(2, dtype=torch.int32, device=x.device)
+    st = _lib.lib().adc_detect_outliers(x.data_ptr(), _DT[x.dtype], rows, cols, float(threshold), 0,
+                                        idx.data_ptr(), status.data_ptr() + 4, status.data_ptr(),
+                                        ws.data_ptr(), ws_bytes, _stream())
+    _lib.check(st, "count_outliers")
+    return status
+
+
 # ---------------------------------------------------------------------------
 # measurement (codec.py:398-429), CUDA events instead of perf_counter
 # ---------------------------------------------------------------------------

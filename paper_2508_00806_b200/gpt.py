@@ -212,6 +212,7 @@ class GPT(nn.Module):
         self.head = nn.Linear(cfg.d_model, cfg.vocab, bias=False)
         self.head.weight = self.wte.weight
         self.apply(self._init)
+        self.channel_scale = None  # policy-evolution drift: per-channel scale of the residual stream
 
     @staticmethod
     def _init(m):
@@ -225,6 +226,8 @@ class GPT(nn.Module):
     def forward(self, idx, targets, pol: ActivationPolicy, seed: int = 0):
         b, s = idx.shape
         x = self.wte(idx) + self.wpe(torch.arange(s, device=idx.device))
+        if self.channel_scale is not None:
+            x = x * self.channel_scale
         with pol.hooks():
             for blk in self.blocks:
                 x = blk(x, pol, seed)

@@ -86,6 +86,8 @@ class ActivationPolicy:
         self._bases: dict[int, _Base] = {}
         self.status: torch.Tensor | None = None
         self.records: dict[int, list] = {}  # op_id -> compressed records of the last step (profiling)
+        self.measure_kinds: frozenset = frozenset()   # tracking iterations: kinds to count outliers of
+        self.measured: dict[int, list] = {}          # op_id -> [device [err, k], cols, rows]
 
     # -- model-facing -------------------------------------------------------
     def tag(self, op_id: int, out: torch.Tensor, fn=None, inputs=()):
@@ -133,6 +135,7 @@ class ActivationPolicy:
         self._tags.clear()
         self._bases.clear()
         self.records = {}
+        self.measured = {}
         if self.status is None:
             self.status = torch.zeros(2, dtype=torch.int32, device="cuda")
         with torch.autograd.graph.saved_tensors_hooks(self.pack, self.unpack):
@@ -152,6 +155,12 @@ class ActivationPolicy:
         op_id, recipe = (tagged[0], tagged[1]) if tagged else (self._current, None)
         if op_id is None:
             return t
+        if (self.measure_kinds and self.ops[op_id].kind in self.measure_kinds and base.is_contiguous()
+                and base.dtype in (torch.bfloat16, torch.float16, torch.float32)):
+            key_m = (op_id, key)
+            if key_m not in self.measured:  # tracking iteration: device outlier count, no sync
+                x = base.reshape(-1, base.shape[-1])
+                self.measured[key_m] = [C.count_outliers_async(x), x.shape[1], x.shape[0]]
         choice = self._choice(op_id)
         if choice == RECOMPUTE and (recipe is None or op_id == 1):
             choice = RETAIN

@@ -102,6 +102,43 @@ def _clone_state(sd):
     return sd
 
 
+def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 4):
+    """Feed the measured peak back into the planner's budget.
+
+    The reference cost model charges only n_layers x per-block activation
+    bytes; transient memory of the chosen mix (a decompressed or recomputed
+    tensor alive during its layer's backward) is not in it.  Solve, run two
+    steps, and if the measured peak exceeds the cap shrink the budget by the
+    overshoot and re-solve (at most ``rounds`` times; MAX over ranks)."""
+    from dataclasses import replace
+    budget = prof.mem_budget_bytes
+    log = []
+    plan = None
+    for _ in range(rounds):
+        p = replace(prof, mem_budget_bytes=max(budget, prof.static_mem_bytes + 1))
+        try:
+            plan = P.solve(p).by_op([o.op_id for o in BLOCK_OPS])
+        except P.InfeasibleError:
+            plan = plan_for("full-recompute")
+        tr.pol.plan = plan
+        tr.model.load_state_dict(snap_model)
+        tr.opt.load_state_dict(_clone_state(snap_opt))
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats(dev)
+        for s in range(2):
+            tr.step(*tr.batch_at(500 + s))
+        torch.cuda.synchronize()
+        peak = torch.tensor([torch.cuda.max_memory_allocated(dev)], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(peak, op=dist.ReduceOp.MAX)
+        peak = int(peak.item())
+        log.append({"budget_bytes": int(budget), "peak_bytes": peak, "plan": plan})
+        if peak <= cap:
+            break
+        budget -= (peak - cap) + (64 << 20)
+    return plan, log
+
+
 def run(args) -> dict:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -141,6 +178,9 @@ def run(args) -> dict:
     snap_opt = _clone_state(tr.opt.state_dict())
     for strategy in args.policy.split(","):
         plan = plan_for(strategy, prof)
+        calib = []
+        if strategy == "adacc" and cap < total_hbm:
+            plan, calib = _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world)
         tr.pol.plan = plan
         tr.model.load_state_dict(snap_model)
         tr.opt.load_state_dict(_clone_state(snap_opt))
@@ -173,8 +213,103 @@ def run(args) -> dict:
             "peak_bytes": peak, "fits_cap": peak <= cap, "final_loss": float(losses[-1].item()),
             "mean_loss": statistics.mean(float(l.item()) for l in losses), "device_error_word": err,
             "compressed_tensors": tr.pol.stats.compressed, "recomputed_tensors": tr.pol.stats.recomputed,
+            "calibration": calib,
         }
         losses_all[strategy] = [float(l.item()) for l in losses]
+    return out
+
+
+def evolve(args) -> dict:
+    """Config 5: policy evolution under a shifting outlier distribution.
+
+    Two arms from the same weights: STATIC keeps the plan solved at iteration
+    1; ADAPTIVE re-profiles the tracked operators on the device at the
+    TrackingSchedule's iterations, re-solves and swaps plans by the reference
+    rule (evolve.py:125-166).  Both see the same drift and batches."""
+    from dataclasses import replace
+    from .evolution import TRACKED_KINDS, OutlierDrift, TrackingSchedule, collect, update_profile
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = GPTConfig.named(args.model)
+    cfg.seq = args.seq or cfg.seq
+    tr = Trainer(cfg, args.batch, rank=rank, world=world, device=dev, ddp=world > 1)
+    cap = int(args.mem_cap_gb * (1 << 30))
+    n = args.evolve
+    drift = OutlierDrift(cols=cfg.d_model, iterations=n, settle_iterations=max(1, args.settle))
+    counts = drift.counts()
+    chans = drift.channels(dev)
+
+    def set_drift(it):
+        scale = torch.ones(cfg.d_model, device=dev, dtype=torch.bfloat16)
+        scale[chans[: int(counts[it - 1])]] = drift.factor
+        tr.model.channel_scale = scale
+
+    tr.pol.plan = plan_for("retain-all")
+    set_drift(1)
+    for s in range(2):
+        tr.step(*tr.batch_at(s))
+    torch.cuda.synchronize()
+    tr.static_after_step = torch.cuda.memory_allocated(dev)
+    t0 = time.perf_counter()
+    tr.step(*tr.batch_at(2))
+    torch.cuda.synchronize()
+    base_ms = (time.perf_counter() - t0) * 1e3
+    prof0, k_caps0 = tr.profile(cap, base_ms)
+    snap_model = {k: v.detach().clone() for k, v in tr.model.state_dict().items()}
+    snap_opt = _clone_state(tr.opt.state_dict())
+    ids = [o.op_id for o in BLOCK_OPS]
+    out = {"model": args.model, "iterations": n, "mem_cap_bytes": cap, "max_interval": args.max_interval,
+           "drift_counts": [int(c) for c in counts[:: max(1, n // 32)]], "arms": {}}
+    for arm in ("static", "adaptive"):
+        tr.model.load_state_dict(snap_model)
+        tr.opt.load_state_dict(_clone_state(snap_opt))
+        tr.step_id = 0
+        prof = prof0
+        plan = P.solve(prof)
+        tr.pol.plan = plan.by_op(ids)
+        tr.pol.k_caps = dict(k_caps0)
+        sched = TrackingSchedule(args.max_interval)
+        log = []
+        ms_total = 0.0
+        torch.cuda.synchronize()
+        for it in range(1, n + 1):
+            set_drift(it)
+            tracked = arm == "adaptive" and sched.is_tracking(it)
+            tr.pol.measure_kinds = TRACKED_KINDS if tracked else frozenset()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            tr.step(*tr.batch_at(5000 + it))
+            b.record()
+            if tracked:
+                measured = collect(tr.pol)  # the one synchronisation of a tracking iteration
+                new_prof, caps = update_profile(prof0, measured)
+                fresh = P.solve(new_prof)
+                incumbent = P.evaluate(new_prof, plan.choices)
+                forced = incumbent.total_bytes > new_prof.mem_budget_bytes
+                adopt = forced or fresh.objective_ms < plan.objective_ms
+                log.append({"iteration": it, "k": {str(k): v[0] for k, v in measured.items()},
+                            "objective_old": plan.objective_ms, "objective_new": fresh.objective_ms,
+                            "forced": forced, "changed": adopt})
+                tr.pol.k_caps.update(caps)
+                if adopt:
+                    plan = fresh
+                    tr.pol.plan = plan.by_op(ids)
+                prof = new_prof
+            b.synchronize()
+            ms_total += a.elapsed_time(b)
+        tokens = args.batch * cfg.seq * world * n
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        out["arms"][arm] = {"tokens_per_s": tokens / (float(t.item()) / 1e3), "final_plan": plan.by_op(ids),
+                            "replans": sum(1 for e in log if e["changed"]), "tracking": log,
+                            "device_error_word": tr.pol.check()}
+    out["improvement_ratio"] = out["arms"]["adaptive"]["tokens_per_s"] / out["arms"]["static"]["tokens_per_s"]
     return out
 
 
@@ -188,8 +323,11 @@ def main(argv=None):
     ap.add_argument("--policy", default="retain-all,adacc")
     ap.add_argument("--mem-cap-gb", type=float, default=0.0)
     ap.add_argument("--profile-out", default="")
+    ap.add_argument("--evolve", type=int, default=0, help="config 5: N iterations of policy evolution")
+    ap.add_argument("--max-interval", type=int, default=64)
+    ap.add_argument("--settle", type=int, default=150)
     args = ap.parse_args(argv)
-    out = run(args)
+    out = evolve(args) if args.evolve else run(args)
     if int(os.environ.get("RANK", "0")) == 0:
         print(json.dumps(out))
     if dist.is_initialized():

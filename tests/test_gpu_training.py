@@ -95,3 +95,21 @@ def test_capped_plan_fits(tiny):
     res = out["results"]["adacc"]
     assert any(v != "retain" for v in res["plan"].values())
     assert res["peak_bytes"] < free
+
+
+def test_policy_evolution_replans(tiny):
+    """Config 5 in miniature: the adaptive arm re-profiles on the device and re-plans."""
+    import argparse
+    from paper_2508_00806_b200 import train
+    args = argparse.Namespace(model="gpt-small-test", batch=8, seq=256, mem_cap_gb=0.0, evolve=40,
+                              max_interval=8, settle=8)
+    # size the cap between the all-outlier and no-outlier regimes
+    free = train.run(argparse.Namespace(model="gpt-small-test", batch=8, seq=256, steps=2, warmup=1,
+                                        policy="retain-all", mem_cap_gb=0.0, profile_out=""))
+    args.mem_cap_gb = free["results"]["retain-all"]["peak_bytes"] * 0.8 / (1 << 30)
+    out = train.evolve(args)
+    ad = out["arms"]["adaptive"]
+    its = [e["iteration"] for e in ad["tracking"]]
+    assert its == [1, 2, 4, 8, 16, 24, 32, 40]
+    assert all(e["k"] for e in ad["tracking"])
+    assert out["arms"]["static"]["tracking"] == []
