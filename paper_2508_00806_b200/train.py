@@ -102,7 +102,7 @@ def _clone_state(sd):
     return sd
 
 
-def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 4):
+def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 6):
     """Feed the measured peak back into the planner's budget.
 
     The reference cost model charges only n_layers x per-block activation
@@ -132,10 +132,16 @@ def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 4)
         if world > 1:
             dist.all_reduce(peak, op=dist.ReduceOp.MAX)
         peak = int(peak.item())
+        same = bool(log) and log[-1]["plan"] == plan
         log.append({"budget_bytes": int(budget), "peak_bytes": peak, "plan": plan})
         if peak <= cap:
             break
-        budget -= (peak - cap) + (64 << 20)
+        # shrink by the overshoot; if the last cut did not change the plan,
+        # cut geometrically harder so the next solve has to move
+        step = (peak - cap) + (64 << 20)
+        if same:
+            step = max(step, 2 * (log[-2]["budget_bytes"] - budget))
+        budget -= step
     return plan, log
 
 
