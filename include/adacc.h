@@ -87,6 +87,13 @@ ADC_API const char *adc_last_error(void);
 ADC_API unsigned long long adc_kernel_launches(void);
 
 /*
+ * Kernel-path selection (tuning / A-B testing; results are identical):
+ *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
+ * Also settable once per process by ADC_COMPRESS_PATH=tma.
+ */
+ADC_API int adc_set_option(const char *key, int value);
+
+/*
  * Closed-form payload size; replaces packed_payload_bytes (codec.py:133-145).
  * Writes the group count, packed-code bytes and total payload bytes (any
  * output pointer may be NULL).  Host-only, no CUDA.

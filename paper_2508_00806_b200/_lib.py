@@ -27,6 +27,7 @@ SIGNATURES = {
     "adc_abi_version": (C.c_int, []),
     "adc_last_error": (C.c_char_p, []),
     "adc_kernel_launches": (C.c_ulonglong, []),
+    "adc_set_option": (C.c_int, [C.c_char_p, C.c_int]),
     "adc_payload_bytes": (C.c_int, [C.c_int, _i64, _i64, _i64, _i64, _P64, _P64, _P64]),
     "adc_workspace_bytes": (_sz, [C.c_int, _i64, _i64, _i64]),
     "adc_compress": (C.c_int, [C.c_int, _vp, C.c_int, _i64, _i64, _i64, C.c_double, _i64,
@@ -63,6 +64,10 @@ def lib() -> C.CDLL:
                 fn.argtypes = args
             _lib = handle
     return _lib
+
+
+def set_option(key: str, value: int) -> None:
+    check(lib().adc_set_option(key.encode(), int(value)), f"set_option({key})")
 
 
 def last_error() -> str:

@@ -2,6 +2,7 @@
 // carving and kernel dispatch.  No allocation, no synchronisation.
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -57,17 +58,16 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   };
   Workspace w;
   const int64_t nodes = node_capacity(cols);
-  w.n_strips = static_cast<int>((cols + 255) / 256);
-  w.counters = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * (w.n_strips + 4)));
+  w.counters = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * 4));
   w.colsum = reinterpret_cast<double *>(take(sizeof(double) * cols));
   w.colmax = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.flag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
-  w.rank = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * cols));
   w.node_lo = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_n = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_left = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
-  w.partial = reinterpret_cast<double *>(take(sizeof(double) * kMaxRowBlocks * cols));
+  w.acc = reinterpret_cast<double *>(take(sizeof(double) * cols));
+  w.macc = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.bytes = off;
   if (ws) *ws = w;
   return off;
@@ -88,6 +88,16 @@ int adc_abi_version(void) { return ADC_ABI_VERSION; }
 const char *adc_last_error(void) { return g_last_error.c_str(); }
 
 unsigned long long adc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int adc_set_option(const char *key, int value) {
+  if (!key) return fail(ADC_EINVAL, "null option key");
+  const std::string k(key);
+  if (k == "compress_path") {  // 1: TMA-fed streaming kernel, 0: register path (default)
+    set_compress_path(value);
+    return ADC_OK;
+  }
+  return fail(ADC_EINVAL, "unknown option");
+}
 
 int adc_payload_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size,
                       int64_t outlier_count, int64_t *n_groups, int64_t *code_bytes,
@@ -152,7 +162,7 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
     workspace_layout(cols, &ws, workspace);
     rc |= launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap,
                               outlier_idx, k_out, err_word, true);
-    rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag, ws.rank,
+    rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag,
                                 outlier_idx, k_out, outlier_val, k_cap, codes, scales, nullptr,
                                 err_word);
     if (rc) return fail(ADC_EINVAL, "outlier dispatch");
@@ -168,7 +178,7 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
     return check_launch("per_channel");
   }
   rc = launch_group_compress(c, x, in_dtype, rows, cols, group_size, asym, nullptr, nullptr,
-                             nullptr, nullptr, nullptr, 0, codes, scales, offsets, err_word);
+                             nullptr, nullptr, 0, codes, scales, offsets, err_word);
   if (rc) return fail(ADC_EINVAL, "group dispatch");
   return check_launch("group_quant");
 }

@@ -9,6 +9,7 @@
 // A group of g = 8*L elements is owned by L adjacent lanes of a warp and
 // reduced with L-wide xor shuffles; every lane derives the group's scale
 // itself (no broadcast), lane 0 of the group stores it.
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -34,36 +35,62 @@ __device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
 }
 
 // Zero the flagged channels of 8 consecutive elements (one row segment,
-// codec.py:328-329) and copy their original f16 values into the (k, rows)
-// side buffer (codec.py:340).  Fully inlined with static indices so the
-// unit's words stay in registers (an out-of-line call forced them through
-// local memory on every unit); the hit branch is rare.
-__device__ __forceinline__ void zero_outlier_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
-                                              const int32_t *__restrict__ rank,
-                                              uint16_t *__restrict__ outl_val, int64_t rows,
-                                              int64_t k_cap, bool bf16_words) {
+// codec.py:328-329).  The flag bytes of the segment are fetched together with
+// the data (zero_flags8) so their latency overlaps the loads; the original
+// values of flagged channels go to the (k, rows) side buffer from dedicated
+// gather CTAs (OutlierSide), not from here: storing them here scattered
+// 2-byte writes across k rows of the buffer and stalled the quantiser on the
+// store queue (ncu, r1).
+__device__ __forceinline__ uint2 zero_flags8(int64_t e, const FastDiv &dc,
+                                             const uint8_t *__restrict__ zflag) {
+  const uint32_t r = fastdiv(static_cast<uint32_t>(e), dc);
+  const uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
+  return __ldg(reinterpret_cast<const uint2 *>(zflag + c));
+}
+__device__ __forceinline__ void zero_apply8(uint32_t *w, uint2 f) {
+  if ((f.x | f.y) != 0) {
+    // byte j of f is 0/1: 16-bit lane j is kept iff its flag is 0
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    uint32_t fb = ((j < 4 ? f.x : f.y) >> (8 * (j & 3))) & 0xffu;
-    if (fb) {
-      uint32_t bits = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-      if (bf16_words) bits = __half_as_ushort(__float2half_rn(__uint_as_float(bits << 16)));
-      int32_t rk = __ldg(rank + c + j);
-      if (rk >= 0 && rk < k_cap) outl_val[static_cast<int64_t>(rk) * rows + r] = bits;
-      w[j >> 1] &= (j & 1) ? 0x0000ffffu : 0xffff0000u;
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t fw = i < 2 ? f.x : f.y;
+      const uint32_t lo = (fw >> (16 * (i & 1))) & 0xffu, hi = (fw >> (16 * (i & 1) + 8)) & 0xffu;
+      w[i] &= (lo ? 0xffff0000u : 0xffffffffu) & (hi ? 0x0000ffffu : 0xffffffffu);
     }
   }
 }
 
-__device__ __forceinline__ void zero_outlier_lanes(uint32_t *w, int64_t e, const FastDiv &dc,
-                                                   const uint8_t *__restrict__ zflag,
-                                                   const int32_t *__restrict__ rank,
-                                                   uint16_t *__restrict__ outl_val, int64_t rows,
-                                                   int64_t k_cap, bool bf16_words) {
-  uint32_t r = fastdiv(static_cast<uint32_t>(e), dc);
-  uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
-  uint2 f = __ldg(reinterpret_cast<const uint2 *>(zflag + c));
-  if ((f.x | f.y) != 0) zero_outlier_hit(w, f, r, c, rank, outl_val, rows, k_cap, bf16_words);
+// Side-buffer gather for the outlier-separated scheme (codec.py:331-341):
+// val[rank][r] = f16(x[r, idx[rank]]).  Run by the first n_gather CTAs of the
+// quantising launch, right after the column statistics, while x is still in
+// L2; threads run along rows (coalesced stores), 8 ranks per thread with
+// their loads issued together.
+struct OutlierSide {
+  const uint32_t *idx;
+  const int32_t *k_dev;
+  int64_t k_cap, rows, cols;
+  uint16_t *val;
+  int n_gather;  // leading CTAs that gather (0: none)
+};
+constexpr int kGatherRanks = 8;
+
+template <int DT>
+__device__ __forceinline__ void gather_side(const void *__restrict__ x, const OutlierSide &o,
+                                            int64_t cta, int64_t n_ctas) {
+  const int64_t k = min(static_cast<int64_t>(*o.k_dev), o.k_cap);
+  const int64_t row_blocks = (o.rows + kThreads - 1) / kThreads;
+  const int64_t items = row_blocks * ((k + kGatherRanks - 1) / kGatherRanks);
+  for (int64_t it = cta; it < items; it += n_ctas) {
+    const int64_t rk0 = (it / row_blocks) * kGatherRanks;
+    const int64_t r = (it % row_blocks) * kThreads + threadIdx.x;
+    if (r >= o.rows) continue;
+    uint16_t v[kGatherRanks];
+#pragma unroll
+    for (int j = 0; j < kGatherRanks; ++j)
+      v[j] = rk0 + j < k ? Loader<DT>::load1(x, r * o.cols + __ldg(o.idx + rk0 + j)) : 0;
+#pragma unroll
+    for (int j = 0; j < kGatherRanks; ++j)
+      if (rk0 + j < k) o.val[(rk0 + j) * o.rows + r] = v[j];
+  }
 }
 
 __device__ __forceinline__ float lo_f(uint32_t w) {
@@ -174,18 +201,26 @@ __device__ __forceinline__ float elem_f16(const void *x, int64_t i) {
 template <int DT, bool ASYM, int L, bool ZERO, int EPL, int U>
 __global__ void __launch_bounds__(kThreads, 4)
     group_quant_fast(const void *__restrict__ x, int64_t n_units, int64_t n_units_pad, FastDiv dc,
-                     int64_t rows, const uint8_t *__restrict__ zflag,
-                     const int32_t *__restrict__ rank, uint16_t *__restrict__ outl_val,
-                     int64_t k_cap, uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
+                     const uint8_t *__restrict__ zflag, OutlierSide side,
+                     uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                      uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
   constexpr int NW = EPL / 2;  // 16-bit pairs per unit
   constexpr int NC = EPL / 8;  // packed code words per unit
   using R = Raw<DT>;
   constexpr bool BF = R::kBf16;
-  const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units_pad;
-       base += step) {
+  int64_t cta = blockIdx.x, n_ctas = gridDim.x;
+  if (ZERO) {
+    if (cta < side.n_gather) {
+      gather_side<DT>(x, side, cta, side.n_gather);
+      return;
+    }
+    cta -= side.n_gather;
+    n_ctas -= side.n_gather;
+  }
+  const int64_t step = n_ctas * kThreads * U;
+  for (int64_t base = cta * kThreads * U; base < n_units_pad; base += step) {
     uint32_t w[U][NW];
+    uint2 zf[U][NC];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t u = base + k * kThreads + threadIdx.x;
@@ -197,17 +232,16 @@ __global__ void __launch_bounds__(kThreads, 4)
         w[k][4 * q + 1] = v.y;
         w[k][4 * q + 2] = v.z;
         w[k][4 * q + 3] = v.w;
+        if (ZERO) zf[k][q] = u < n_units ? zero_flags8(u * EPL + 8 * q, dc, zflag) : make_uint2(0, 0);
       }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t u = base + k * kThreads + threadIdx.x;
       const bool act = u < n_units;
-      if (ZERO && act) {
+      if (ZERO) {
 #pragma unroll
-        for (int q = 0; q < NC; ++q)
-          zero_outlier_lanes(&w[k][4 * q], u * EPL + 8 * q, dc, zflag, rank, outl_val, rows, k_cap,
-                             BF);
+        for (int q = 0; q < NC; ++q) zero_apply8(&w[k][4 * q], zf[k][q]);
       }
       uint16_t s_bits, o_bits = 0;
       bool bad, native = true;
@@ -444,17 +478,11 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Stand-alone side-buffer gather (generic path and the TMA variant).
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
-    outlier_gather_generic(const void *__restrict__ x, const uint32_t *__restrict__ idx,
-                           const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows,
-                           int64_t cols, uint16_t *__restrict__ outl_val) {
-  const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < k * rows;
-       t += static_cast<int64_t>(gridDim.x) * kThreads) {
-    const int64_t i = t / rows, r = t - i * rows;
-    outl_val[t] = Loader<DT>::load1(x, r * cols + idx[i]);
-  }
+    outlier_gather(const void *__restrict__ x, OutlierSide side) {
+  gather_side<DT>(x, side, blockIdx.x, gridDim.x);
 }
 
 template <int OT, bool ASYM>
@@ -491,14 +519,19 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
+static std::atomic<int> g_compress_path{-1};
+
 bool use_tma_compress() {
-  static int v = -1;
+  int v = g_compress_path.load(std::memory_order_relaxed);
   if (v < 0) {
     const char *e = getenv("ADC_COMPRESS_PATH");
     v = (e && e[0] == 't') ? 1 : 0;  // measured: the register path is faster for now
+    g_compress_path.store(v, std::memory_order_relaxed);
   }
   return v == 1;
 }
+
+void set_compress_path(int v) { g_compress_path.store(v ? 1 : 0, std::memory_order_relaxed); }
 
 static inline int grid_for(const Ctx &c, int64_t work_items, int per_block) {
   int64_t need = (work_items + per_block - 1) / per_block;
@@ -539,9 +572,19 @@ static inline int lanes_for_group(int64_t g, int epl) {
 
 constexpr int kUnroll = 2;
 
+// Gather work: (k_cap / 8) rank blocks x (rows / 256) row blocks, at most
+// one CTA per SM (the gather is latency-bound and short).
+static OutlierSide outlier_side(const Ctx &c, const uint32_t *idx, const int32_t *k_dev,
+                                int64_t k_cap, int64_t rows, int64_t cols, uint16_t *val) {
+  OutlierSide o{idx, k_dev, k_cap, rows, cols, val, 0};
+  if (k_cap <= 0 || !val || !idx || !k_dev) return o;
+  const int64_t items = ((rows + kThreads - 1) / kThreads) * ((k_cap + kGatherRanks - 1) / kGatherRanks);
+  o.n_gather = static_cast<int>(items < c.num_sms ? items : c.num_sms);
+  return o;
+}
+
 int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                          int64_t g, bool asym, const uint8_t *zero_flag, const int32_t *rank,
-                          const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
+                          int64_t g, bool asym, const uint8_t *zero_flag, const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
                           int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
                           uint32_t *err) {
   const int64_t n = rows * cols;
@@ -549,10 +592,14 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
   const bool zero = zero_flag != nullptr;
   const bool zero_ok = !zero || (cols % 8 == 0 && n < (1ll << 31));
   const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
+  const OutlierSide side = outlier_side(c, idx, k_dev, zero ? k_cap : 0, rows, cols, outl_val);
   int L = pc ? 0 : lanes_for_group(g, 8);
-  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok)
-    return launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, rank, outl_val,
-                                     k_cap, codes, scales, offsets, err);
+  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok) {
+    const int rc = launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, codes,
+                                             scales, offsets, err);
+    if (rc || !zero) return rc;
+    return launch_outlier_gather(c, x, dt, idx, k_dev, k_cap, rows, cols, outl_val);
+  }
   L = pc ? 0 : lanes_for_group(g, 16);
   if (L > 0 && n % 16 == 0 && aligned(x, 16) && aligned(codes, 8) && zero_ok) {
     const int64_t n_units = n / 16;
@@ -562,16 +609,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
         group_quant_fast<DT, true, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
-            offsets, err), note_launches(1);
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, zero_flag, rank, outl_val, k_cap, codes32, scales,
-            nullptr, err), note_launches(1);
+        group_quant_fast<DT, false, LL, true, 16, kUnroll><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
         group_quant_fast<DT, false, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
-            nullptr, err), note_launches(1);
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
     return 0;
@@ -585,16 +629,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
         group_quant_fast<DT, true, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
-            offsets, err), note_launches(1);
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, zero_flag, rank, outl_val, k_cap, codes32, scales,
-            nullptr, err), note_launches(1);
+        group_quant_fast<DT, false, LL, true, 8, kUnroll><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
         group_quant_fast<DT, false, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
-            x, n_units, n_units_pad, dc, rows, nullptr, nullptr, nullptr, 0, codes32, scales,
-            nullptr, err), note_launches(1);
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
     return 0;
@@ -625,10 +666,10 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                           uint16_t *outl_val) {
-  if (k_cap <= 0) return 0;
-  const int grid = grid_for(c, k_cap * rows, kThreads);
-  ADC_DT_SWITCH(dt, DT, outlier_gather_generic<DT><<<grid, kThreads, 0, c.stream>>>(
-                            x, idx, k_dev, k_cap, rows, cols, outl_val), note_launches(1));
+  const OutlierSide side = outlier_side(c, idx, k_dev, k_cap, rows, cols, outl_val);
+  if (side.n_gather == 0) return 0;
+  ADC_DT_SWITCH(dt, DT, outlier_gather<DT><<<side.n_gather, kThreads, 0, c.stream>>>(x, side),
+                note_launches(1));
   return 0;
 }
 

@@ -33,15 +33,13 @@ struct Ctx {
 
 // Workspace carving (offsets in bytes, 256-aligned).  Must be zero-filled
 // once by the caller; the kernels leave every counter at zero on exit.
-constexpr int kMaxRowBlocks = 128;  // gy cap of the column-statistics kernel
 struct Workspace {
   double *colsum;        // cols       column |x| sums (outlier)
   uint32_t *colmax;      // cols       column abs-max f16 bits (per-channel)
   uint8_t *flag;         // cols + 8   outlier flags
-  int32_t *rank;         // cols       outlier rank of a flagged column, else -1
-  double *partial;       // kMaxRowBlocks * cols per-CTA column partials
-  uint32_t *counters;    // n_strips + 4 arrival counters / flags
-  int n_strips;
+  double *acc;           // cols       f64 atomic column-sum accumulators (zero at rest)
+  uint32_t *macc;        // cols       u32 atomic column-max accumulators (zero at rest)
+  uint32_t *counters;    // 4          arrival counters (zero at rest)
   int32_t *node_lo;      // pairwise-tree nodes (used when cols > 16384)
   int32_t *node_n;
   int32_t *node_left;
@@ -53,8 +51,7 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base);
 
 // group kernels (group.cu)
 int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                          int64_t g, bool asym, const uint8_t *zero_flag, const int32_t *rank,
-                          const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
+                          int64_t g, bool asym, const uint8_t *zero_flag, const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
                           int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
                           uint32_t *err);
 int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
@@ -67,11 +64,11 @@ int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *va
 // TMA-fed streaming variant of the fast group compress (stream.cu); L = lanes
 // per group at 8 elements per lane.
 int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                              int L, bool asym, const uint8_t *zero_flag, const int32_t *rank,
-                              uint16_t *outl_val, int64_t k_cap, uint8_t *codes, uint16_t *scales,
-                              uint16_t *offsets, uint32_t *err);
+                              int L, bool asym, const uint8_t *zero_flag, uint8_t *codes,
+                              uint16_t *scales, uint16_t *offsets, uint32_t *err);
 // Tuning switch read once from the environment: ADC_COMPRESS_PATH=tma|regs (default regs).
 bool use_tma_compress();
+void set_compress_path(int v);
 
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,

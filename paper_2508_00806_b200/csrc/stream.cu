@@ -49,29 +49,20 @@ __device__ __forceinline__ uint32_t fdiv_u32(uint32_t n, const FastDiv &f) {
   return static_cast<uint32_t>((static_cast<uint64_t>(n) * f.m) >> f.p);
 }
 
-// rare path of the outlier zeroing: copy + zero flagged lanes of one unit
-__device__ __forceinline__ void stream_zero_hit(uint32_t *w, uint2 f, uint32_t r, uint32_t c,
-                                             const int32_t *__restrict__ rank,
-                                             uint16_t *__restrict__ outl_val, int64_t rows,
-                                             int64_t k_cap) {
+// rare path of the outlier zeroing (values are gathered separately)
+__device__ __forceinline__ void stream_zero_hit(uint32_t *w, uint2 f) {
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     const uint32_t fb = ((j < 4 ? f.x : f.y) >> (8 * (j & 3))) & 0xffu;
-    if (fb) {
-      const uint32_t bits = (w[j >> 1] >> (16 * (j & 1))) & 0xffffu;
-      const int32_t rk = __ldg(rank + c + j);
-      if (rk >= 0 && rk < k_cap) outl_val[static_cast<int64_t>(rk) * rows + r] = bits;
-      w[j >> 1] &= (j & 1) ? 0x0000ffffu : 0xffff0000u;
-    }
+    if (fb) w[j >> 1] &= (j & 1) ? 0x0000ffffu : 0xffff0000u;
   }
 }
 
 template <int DT, bool ASYM, int L, bool ZERO>
 __global__ void __launch_bounds__(kStreamThreads, 2)
     group_quant_tma(const void *__restrict__ x, int64_t n, int64_t n_units, int64_t n_units_pad,
-                    FastDiv dc, int64_t rows, const uint8_t *__restrict__ zflag,
-                    const int32_t *__restrict__ rank, uint16_t *__restrict__ outl_val,
-                    int64_t k_cap, uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
+                    FastDiv dc, const uint8_t *__restrict__ zflag,
+                    uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                     uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
@@ -128,7 +119,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2)
         const uint32_t r = fdiv_u32(e, dc);
         const uint32_t c = e - r * dc.d;
         const uint2 f = __ldg(reinterpret_cast<const uint2 *>(zflag + c));
-        if ((f.x | f.y) != 0) stream_zero_hit(w, f, r, c, rank, outl_val, rows, k_cap);
+        if ((f.x | f.y) != 0) stream_zero_hit(w, f);
       }
       uint16_t s_bits, o_bits = 0;
       bool bad;
@@ -223,8 +214,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2)
 
 template <int DT, bool ASYM, int L, bool ZERO>
 static int launch_one(const Ctx &c, const void *x, int64_t n, int64_t n_units, int64_t n_units_pad,
-                      FastDiv dc, int64_t rows, const uint8_t *zflag, const int32_t *rank,
-                      uint16_t *outl_val, int64_t k_cap, uint32_t *codes, uint16_t *scales,
+                      FastDiv dc, const uint8_t *zflag, uint32_t *codes, uint16_t *scales,
                       uint16_t *offsets, uint32_t *err) {
   static bool configured = false;  // per template instance
   if (!configured) {
@@ -238,15 +228,14 @@ static int launch_one(const Ctx &c, const void *x, int64_t n, int64_t n_units, i
   int64_t grid = static_cast<int64_t>(c.num_sms) * 2;
   if (grid > n_tiles) grid = n_tiles;
   group_quant_tma<DT, ASYM, L, ZERO><<<static_cast<int>(grid), kStreamThreads, kStreamSmem, c.stream>>>(
-      x, n, n_units, n_units_pad, dc, rows, zflag, rank, outl_val, k_cap, codes, scales, offsets, err);
+      x, n, n_units, n_units_pad, dc, zflag, codes, scales, offsets, err);
   note_launches(1);
   return 0;
 }
 
 int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                              int L, bool asym, const uint8_t *zero_flag, const int32_t *rank,
-                              uint16_t *outl_val, int64_t k_cap, uint8_t *codes, uint16_t *scales,
-                              uint16_t *offsets, uint32_t *err) {
+                              int L, bool asym, const uint8_t *zero_flag, uint8_t *codes,
+                              uint16_t *scales, uint16_t *offsets, uint32_t *err) {
   const int64_t n = rows * cols;
   const int64_t n_units = n / 8;
   const int64_t n_units_pad = (n_units + L - 1) / L * L;
@@ -255,14 +244,14 @@ int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows,
   int rc = 0;
   ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
     if (asym)
-      rc = launch_one<DT, true, LL, false>(c, x, n, n_units, n_units_pad, dc, rows, nullptr, nullptr,
-                                           nullptr, 0, c32, scales, offsets, err);
+      rc = launch_one<DT, true, LL, false>(c, x, n, n_units, n_units_pad, dc, nullptr, c32, scales,
+                                           offsets, err);
     else if (zero_flag)
-      rc = launch_one<DT, false, LL, true>(c, x, n, n_units, n_units_pad, dc, rows, zero_flag, rank,
-                                           outl_val, k_cap, c32, scales, nullptr, err);
+      rc = launch_one<DT, false, LL, true>(c, x, n, n_units, n_units_pad, dc, zero_flag, c32, scales,
+                                           nullptr, err);
     else
-      rc = launch_one<DT, false, LL, false>(c, x, n, n_units, n_units_pad, dc, rows, nullptr, nullptr,
-                                            nullptr, 0, c32, scales, nullptr, err);
+      rc = launch_one<DT, false, LL, false>(c, x, n, n_units, n_units_pad, dc, nullptr, c32, scales,
+                                            nullptr, err);
   }));
   return rc;
 }

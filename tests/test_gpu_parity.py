@@ -257,3 +257,19 @@ def test_bf16_overflow_is_nonfinite(torch_cuda):
                  adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), adc.SchemeSpec(adc.Scheme.SYMMETRIC_GROUP, 0)):
         with pytest.raises(adc.NonFiniteInputError):
             adc.compress(x, spec)
+
+
+@pytest.mark.parametrize("shape", [(64, 768), (8192, 768), (1000, 1000), (4096, 4096), (2048, 11008),
+                                   (333, 1024), (8192, 1024), (3, 20000)])
+@pytest.mark.parametrize("dtype_name", ["bfloat16", "float32"])
+def test_outlier_separated_wide_shapes(torch_cuda, shape, dtype_name):
+    """K4 at layer widths and ragged row counts (full-wave column reduction, heap tree, gather)."""
+    torch = torch_cuda
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    x = rng.normal(size=shape).astype(np.float32)
+    hot = rng.choice(shape[1], max(1, shape[1] // 64), replace=False)
+    x[:, hot] *= rng.uniform(10, 60)
+    xt = torch.from_numpy(x).to(getattr(torch, dtype_name))
+    want = oracle_run(xt.to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+    got = device_run(xt, cases.OUTL, 128, 3.0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
