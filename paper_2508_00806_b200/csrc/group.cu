@@ -165,7 +165,7 @@ __device__ __forceinline__ void unit_codes_exact(const uint32_t *w, float s, flo
 //   large offset -> float64, as codec.py:223-231);
 //   r = Markstein-refined d/s; within 2^-20 of a half-integer b the exact
 //   residual d - b*s (one FMA, exact here) decides, ties to even.
-__device__ __noinline__ int asym_exact_code(float h, float s, float inv, float o) {
+__device__ __forceinline__ int asym_exact_code(float h, float s, float inv, float o) {
   const float d = h - o;
   const float bb = d - h;
   const float err = (h - (d - bb)) + (-o - bb);
@@ -181,18 +181,31 @@ __device__ __noinline__ int asym_exact_code(float h, float s, float inv, float o
   if (fabsf(fabsf(fr) - 0.5f) < 0x1p-20f) {
     const float bnd = c + (fr > 0.f ? 0.5f : -0.5f);  // nearest half-integer
     const float res = fmaf(-bnd, s, d);               // exact sign of q - bnd
-    const float up = bnd + 0.5f, dn = bnd - 0.5f;
-    const float even = (fmodf(up, 2.f) == 0.f) ? up : dn;
-    code = static_cast<int>(res > 0.f ? up : (res < 0.f ? dn : even));
+    const int up = static_cast<int>(bnd + 0.5f), dn = up - 1;
+    code = res > 0.f ? up : (res < 0.f ? dn : ((up & 1) == 0 ? up : dn));  // ties to even
   }
   return min(max(code, -8), 7);
 }
 
-// f16 value (as float) of element i of the input, re-read from global memory
-// (the rare exact path only).
-template <int DT>
-__device__ __forceinline__ float elem_f16(const void *x, int64_t i) {
-  return h2f(Loader<DT>::load1(x, i));
+// Word j (runtime) of a unit held in registers: a selp tree, so the unit
+// stays in registers (an indexed access would go through local memory).
+__device__ __forceinline__ uint32_t selp_u32(bool c, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.b32 %0, %1, %2, p;\n\t}"
+      : "=r"(r) : "r"(a), "r"(b), "r"(static_cast<uint32_t>(c)));
+  return r;
+}
+template <int NW>
+__device__ __forceinline__ uint32_t mux_word(const uint32_t *w, int j) {
+  if (NW == 4) {
+    const uint32_t a = selp_u32(j & 1, w[1], w[0]), b = selp_u32(j & 1, w[3], w[2]);
+    return selp_u32(j & 2, b, a);
+  } else {
+    const uint32_t a = selp_u32(j & 1, w[1], w[0]), b = selp_u32(j & 1, w[3], w[2]);
+    const uint32_t c = selp_u32(j & 1, w[5 % NW], w[4 % NW]), d = selp_u32(j & 1, w[7 % NW], w[6 % NW]);
+    const uint32_t ab = selp_u32(j & 2, b, a), cd = selp_u32(j & 2, d, c);
+    return selp_u32(j & 4, cd, ab);
+  }
 }
 
 // Fast group kernel: a lane owns EPL (8 or 16) consecutive elements, a group
@@ -244,6 +257,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         for (int q = 0; q < NC; ++q) zero_apply8(&w[k][4 * q], zf[k][q]);
       }
       uint16_t s_bits, o_bits = 0;
+      uint32_t lo_bits = 0;  // asymmetric: the group minimum (f16 bits)
       bool bad, native = true;
       if (ASYM) {
         // packed max/min (NaN-propagating) in the input's own 16-bit format
@@ -273,6 +287,7 @@ __global__ void __launch_bounds__(kThreads, 4)
         }
         bad = ((hi & 0x7fffu) >= 0x7c00u) || ((lo & 0x7fffu) >= 0x7c00u);
         asym_params(hi, lo, o_bits, s_bits);
+        lo_bits = lo;
       } else {
         uint32_t m = 0;
         if (act) {
@@ -301,21 +316,46 @@ __global__ void __launch_bounds__(kThreads, 4)
       uint32_t fix = 0;  // elements whose fast quotient is within the tie margin
       if (ASYM) {
         const QParams q = make_qparams(s_bits, o_bits);
-        // r is within 2^-18.8 of the exact quotient of the f16 value; for bf16
-        // the native x differs from f16(x) by <= 2^-25 (tiny values only), i.e.
-        // by <= 2^-25/s in the quotient.  Elements inside that margin of a
-        // half-integer are redone exactly after packing.
-        const float thr = 0.5f - (0x1p-17f + (BF ? 0x1p-25f * q.inv : 0.f));
-#pragma unroll
-        for (int i = 0; i < NW; ++i) {
-#pragma unroll
-          for (int hh = 0; hh < 2; ++hh) {
-            const float xv = hh ? R::hi(w[k][i]) : R::lo(w[k][i]);
-            const float r = fminf(fmaxf((xv - q.o) * q.inv, -8.f), 7.f);
-            const float tv = r + kMagic8;
-            fix |= (fabsf(r - (tv - kMagic8)) > thr ? 1u : 0u) << (2 * i + hh);
-            t[2 * i + hh] = __float_as_uint(tv);
+        // r = RN(x*inv - RN(o*inv)) (one FFMA) is within 2^-19 + |o*inv|*2^-23
+        // of the exact quotient (x - o)/s of the f16 value (inv: 1-ulp
+        // reciprocal); for bf16 the native x differs from f16(x) by <= 2^-25
+        // (tiny values only), i.e. by <= 2^-25/s in the quotient.  Elements
+        // within that margin (doubled) of a half-integer are redone exactly.
+        const float oi = q.o * q.inv;
+        const float thr = 0.5f - (0x1p-17f + fabsf(oi) * 0x1p-22f + (BF ? 0x1p-25f * q.inv : 0.f));
+        // the lower clip only matters for degenerate groups whose minimum
+        // quotient can fall below -8.5 (f16 rounding of a large offset)
+        const bool clip_lo = fmaf(h2f(lo_bits), q.inv, -oi) < -8.f;
+        // two elements per FFMA2 / FADD2; rounding residuals |e| beyond thr
+        // mark the elements redone exactly (frequent for bf16 data, whose
+        // coarse mantissas make exact half-integer quotients common)
+        const uint64_t inv2 = f2_pack(q.inv, q.inv), noi2 = f2_pack(-oi, -oi);
+        const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
+        auto pair = [&](int i, bool lo_clip) {
+          float rl, rh;
+          f2_unpack(f2_fma(f2_pack(R::lo(w[k][i]), R::hi(w[k][i])), inv2, noi2), rl, rh);
+          rl = fminf(rl, 7.f);
+          rh = fminf(rh, 7.f);
+          if (lo_clip) {
+            rl = fmaxf(rl, -8.f);
+            rh = fmaxf(rh, -8.f);
           }
+          const uint64_t r2 = f2_pack(rl, rh);
+          const uint64_t tv2 = f2_add(r2, mg2);
+          float el, eh, tl, th;
+          f2_unpack(f2_sub(r2, f2_sub(tv2, mg2)), el, eh);
+          f2_unpack(tv2, tl, th);
+          fix |= (fabsf(el) > thr ? 1u : 0u) << (2 * i);
+          fix |= (fabsf(eh) > thr ? 1u : 0u) << (2 * i + 1);
+          t[2 * i] = __float_as_uint(tl);
+          t[2 * i + 1] = __float_as_uint(th);
+        };
+        if (__any_sync(__activemask(), clip_lo)) {  // degenerate groups only
+#pragma unroll
+          for (int i = 0; i < NW; ++i) pair(i, true);
+        } else {
+#pragma unroll
+          for (int i = 0; i < NW; ++i) pair(i, false);
         }
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
@@ -340,15 +380,23 @@ __global__ void __launch_bounds__(kThreads, 4)
       if (ASYM) {
         const float sc = h2f(s_bits), so = h2f(o_bits);
         const float scd = sc == 0.f ? 1.f : sc, inv = rcp_approx(scd);
-        while (fix) {  // per-lane, proportional to the number of near-ties
-          const int i = __ffs(fix) - 1;
-          fix &= fix - 1;
-          const int code = asym_exact_code(elem_f16<DT>(x, u * EPL + i), scd, inv, so);
-          const uint32_t sh = 4 * (i & 7), nib = static_cast<uint32_t>(code) & 0xfu;
-          if (i < 8)
-            c0 = (c0 & ~(0xfu << sh)) | (nib << sh);
-          else
-            c1 = (c1 & ~(0xfu << sh)) | (nib << sh);
+        // one near-tie element per lane per round, all lanes together: the
+        // warp pays max(popcount(fix)) rounds (usually one) instead of one
+        // divergent pass per element position
+        while (__any_sync(__activemask(), fix != 0)) {
+          if (fix) {
+            const int i = __ffs(fix) - 1;
+            fix &= fix - 1;
+            const uint32_t word = mux_word<NW>(w[k], i >> 1);
+            const uint32_t raw = (word >> (16 * (i & 1))) & 0xffffu;
+            const int code = asym_exact_code(h2f(BF ? bf16_bits_to_f16_bits(raw) : raw), scd, inv, so);
+            const uint32_t sh = 4 * (i & 7), nib = static_cast<uint32_t>(code) & 0xfu;
+            const uint32_t m = ~(0xfu << sh), v = nib << sh;
+            if (i < 8)
+              c0 = (c0 & m) | v;
+            else
+              c1 = (c1 & m) | v;
+          }
         }
       }
       if (NC == 1) {

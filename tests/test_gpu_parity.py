@@ -273,3 +273,48 @@ def test_outlier_separated_wide_shapes(torch_cuda, shape, dtype_name):
     want = oracle_run(xt.to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
     got = device_run(xt, cases.OUTL, 128, 3.0)
     assert cases.norm_digest(*got) == cases.norm_digest(*want)
+
+
+@pytest.mark.parametrize("scheme,group", [(cases.OUTL, 128), (cases.ASYM, 128), (cases.SYM, 0)])
+def test_graph_replay_matches_eager(torch_cuda, scheme, group):
+    """bench.py times CUDA-graph replays of the codec calls: replays (which
+    reuse the self-resetting workspace) must reproduce the eager bytes."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200.slots import CodecSlot
+    rows, cols = 2048, 1024
+    g = torch.Generator(device="cuda").manual_seed(3)
+    xs = [torch.randn(rows, cols, device="cuda", generator=g).to(torch.bfloat16) for _ in range(2)]
+    for x in xs:
+        x[:, ::97] *= 40
+    spec = adc.SchemeSpec(adc.Scheme(scheme), group)
+    slot = CodecSlot(rows, cols, spec, torch.bfloat16, torch.bfloat16, k_cap=64)
+    y = torch.empty(rows, cols, dtype=torch.bfloat16, device="cuda")
+
+    def snapshot():
+        parts = [slot.codes.clone()]
+        parts += [t.clone() for t in (slot.scales, slot.offsets, slot.idx, slot.val) if t is not None]
+        parts.append(y.clone())
+        return parts
+
+    eager = []
+    for x in xs:
+        slot.compress_ptr(x.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        slot.decompress_ptr(y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        eager.append(snapshot())
+    src = torch.empty_like(xs[0])
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        sp = torch.cuda.current_stream().cuda_stream
+        slot.compress_ptr(src.data_ptr(), sp)
+        slot.decompress_ptr(y.data_ptr(), sp)
+    for rep in range(3):
+        for x, want in zip(xs, eager):
+            src.copy_(x)
+            graph.replay()
+            torch.cuda.synchronize()
+            got = snapshot()
+            for a, b in zip(got, want):
+                assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
+    assert int(slot.status[0]) == 0
