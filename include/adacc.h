@@ -89,9 +89,20 @@ ADC_API unsigned long long adc_kernel_launches(void);
 /*
  * Kernel-path selection (tuning / A-B testing; results are identical):
  *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
+ *   "outlier_path"  1 = single-launch cooperative outlier-separated compress
+ *                   (where eligible), 2 = column-statistics launch + quantiser
+ *                   launch (default: measured faster).  Also ADC_OUTLIER_PATH=1.
  * Also settable once per process by ADC_COMPRESS_PATH=tma.
  */
 ADC_API int adc_set_option(const char *key, int value);
+
+/*
+ * Tuning aid: with adc_set_option("trace", 1), the single-launch
+ * outlier-separated kernel records per-CTA phase timestamps; this copies the
+ * last launch's records (8 u64 per CTA: globaltimer at entry, then clock64
+ * deltas at the end of each phase) to host memory.  Returns the count copied.
+ */
+ADC_API int adc_debug_trace(unsigned long long *out, int n);
 
 /*
  * Closed-form payload size; replaces packed_payload_bytes (codec.py:133-145).

@@ -68,6 +68,7 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
   w.acc = reinterpret_cast<double *>(take(sizeof(double) * cols));
   w.macc = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
+  w.pflag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
   w.bytes = off;
   if (ws) *ws = w;
   return off;
@@ -96,7 +97,21 @@ int adc_set_option(const char *key, int value) {
     set_compress_path(value);
     return ADC_OK;
   }
+  if (k == "trace") {  // record phase timestamps of the fused kernel (adc_debug_trace)
+    set_fused_trace(value);
+    return ADC_OK;
+  }
+  if (k == "outlier_path") {  // 1: single-launch fused kernel (default), 2: colreduce + quantiser
+    set_fused_outlier(value == 1);
+    return ADC_OK;
+  }
   return fail(ADC_EINVAL, "unknown option");
+}
+
+int adc_debug_trace(unsigned long long *out, int n) {
+  if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
+  const int r = read_fused_trace(out, n);
+  return r < 0 ? fail(ADC_ECUDA, "trace copy failed") : r;
 }
 
 int adc_payload_bytes(int scheme, int64_t rows, int64_t cols, int64_t group_size,
@@ -160,6 +175,9 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
       return fail(ADC_EWORKSPACE, "workspace too small");
     Workspace ws;
     workspace_layout(cols, &ws, workspace);
+    if (launch_outlier_fused(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
+                             codes, scales, outlier_idx, outlier_val, k_out, err_word))
+      return check_launch("outlier_fused");
     rc |= launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap,
                               outlier_idx, k_out, err_word, true);
     rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag,

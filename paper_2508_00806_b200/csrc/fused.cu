@@ -1,0 +1,728 @@
+// K4 in ONE launch: the outlier-separated compressor (codec.py:308-341) as a
+// persistent cooperative kernel, one CTA per SM, the input read from HBM once.
+//
+//   A. Each CTA owns a contiguous, group-aligned slice of the flattened
+//      matrix.  Its leading part (as much as fits in shared memory) is pulled
+//      into shared memory by bulk copies (cp.async.bulk, the TMA engine) issued
+//      by one thread at kernel entry -- the whole slice is in flight at once;
+//      the rest is streamed with 128-bit loads marked L2 evict_last.  Every
+//      thread owns one 8-column unit (fixed column across its rows), so its
+//      eight float64 |x| partial sums stay in registers; the row lanes are
+//      folded in shared memory and added to the column accumulators with f64
+//      atomics (exact, see outlier.cu).
+//   B. Grid barrier (arrive / depart counters, zero at rest).  Every CTA then
+//      reads the column sums and evaluates mean / std / z / ranks itself
+//      (stats.cuh; the same numpy pairwise tree as the two-launch path), so no
+//      CTA waits on a single finisher; CTA 0 publishes k and the indices; the
+//      last CTA to depart re-zeroes the accumulators.
+//   C. Each CTA quantises its own slice -- from shared memory for the resident
+//      part, from L2 for the streamed rest -- with the flagged channels zeroed
+//      (codec.py:328-330), and gathers the original float16 values of the
+//      flagged channels of its rows into the (k, rows) side buffer (:339-340).
+//
+// Eligibility (host side, launch_outlier_fused): cols % 8 == 0, cols <= 4096,
+// group size g = 8L with L a power of two <= 32, n % g == 0, aligned buffers,
+// cooperative launch available.  Otherwise the caller uses the two-launch
+// path (colreduce + group_quant_fast), which produces identical bytes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdlib>
+#include <functional>
+#include <vector>
+
+#include "common.cuh"
+#include "launch.h"
+#include "quant.cuh"
+#include "stats.cuh"
+
+namespace adc {
+
+constexpr int kFT = 512;             // threads per CTA
+constexpr int kFChunk = 32768;       // bulk-copy chunk (one mbarrier each)
+constexpr int kFMaxChunks = 8;
+constexpr int kFMaxCols = 8 * kFT;   // one 8-column unit per thread in phase A
+constexpr double kFExact = 536870912.0;  // 2^29
+
+struct FusedArgs {
+  const void *x;
+  int64_t rows, cols, n_groups;
+  int cu;            // cols / 8
+  int stride;        // phase-A unit stride: (kFT / cu) * cu
+  int res_units;     // resident units per CTA (shared-memory tile capacity)
+  int tile_bytes;
+  int kidx_cap;      // shared index capacity = min(k_cap, cols)
+  double thr;
+  int64_t k_cap;
+  double *acc;       // [cols] f64 column accumulators, zero at rest
+  uint32_t *cnt;     // [0] arrive, [1] depart (zero at rest)
+  uint32_t *codes;
+  uint16_t *scales;
+  uint32_t *idx;
+  uint16_t *val;
+  int32_t *k_out;
+  uint32_t *err;
+  uint8_t *pflag;    // [cols + 8] previous call's flags: the speculated channel set
+  int spec;          // speculate in phase A (cols % g == 0: groups never straddle rows)
+  int trace;         // record per-CTA phase timestamps into g_ftrace (tuning)
+  PwTree tree;       // numpy's pairwise-sum tree for n = cols (host-built)
+};
+
+// Phase timestamps of the last traced launch: per CTA, [0] globaltimer at
+// entry, [1..6] clock64 deltas at the ends of: A, atomics, barrier,
+// statistics, quantisation, gather.
+constexpr int kTraceSlots = 16;  // [0] globaltimer, [1..7] phase ends, [8..] sub-phases
+constexpr int kTraceCtas = 1024;
+__device__ unsigned long long g_ftrace[kTraceCtas * kTraceSlots];
+#define FTRACE_BY(slot, who)                                                                 \
+  do {                                                                                       \
+    if (a.trace && tid == (who) && b < kTraceCtas)                                           \
+      g_ftrace[b * kTraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - t_0); \
+  } while (0)
+#define FTRACE(slot)                                                                         \
+  do {                                                                                       \
+    if (a.trace && tid == 0 && b < kTraceCtas)                                               \
+      g_ftrace[b * kTraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - t_0); \
+  } while (0)
+
+template <int DT>
+struct FTile;  // 8 elements of a resident tile as f16 words (colsum) / raw words (quant)
+template <>
+struct FTile<ADC_BF16> {
+  static constexpr int kUB = 16;
+  __device__ __forceinline__ static uint4 raw(const unsigned char *p) { return *reinterpret_cast<const uint4 *>(p); }
+  __device__ __forceinline__ static uint4 f16(const unsigned char *p) {
+    const uint4 v = raw(p);
+    return make_uint4(bf2_to_h2(v.x), bf2_to_h2(v.y), bf2_to_h2(v.z), bf2_to_h2(v.w));
+  }
+  __device__ __forceinline__ static uint16_t one(const unsigned char *p) {
+    return static_cast<uint16_t>(bf16_bits_to_f16_bits(*reinterpret_cast<const uint16_t *>(p)));
+  }
+};
+template <>
+struct FTile<ADC_F16> {
+  static constexpr int kUB = 16;
+  __device__ __forceinline__ static uint4 raw(const unsigned char *p) { return *reinterpret_cast<const uint4 *>(p); }
+  __device__ __forceinline__ static uint4 f16(const unsigned char *p) { return raw(p); }
+  __device__ __forceinline__ static uint16_t one(const unsigned char *p) { return *reinterpret_cast<const uint16_t *>(p); }
+};
+template <>
+struct FTile<ADC_F32> {
+  static constexpr int kUB = 32;
+  __device__ __forceinline__ static uint4 f16(const unsigned char *p) {
+    const uint4 a = *reinterpret_cast<const uint4 *>(p), b = *reinterpret_cast<const uint4 *>(p + 16);
+    return make_uint4(f32x2_to_h2(__uint_as_float(a.x), __uint_as_float(a.y)),
+                      f32x2_to_h2(__uint_as_float(a.z), __uint_as_float(a.w)),
+                      f32x2_to_h2(__uint_as_float(b.x), __uint_as_float(b.y)),
+                      f32x2_to_h2(__uint_as_float(b.z), __uint_as_float(b.w)));
+  }
+  __device__ __forceinline__ static uint4 raw(const unsigned char *p) { return f16(p); }
+  __device__ __forceinline__ static uint16_t one(const unsigned char *p) {
+    return __half_as_ushort(__float2half_rn(*reinterpret_cast<const float *>(p)));
+  }
+};
+
+// raw words of 8 elements from global memory (phase C re-read, L2 hits)
+template <int DT>
+__device__ __forceinline__ uint4 f_global_raw(const void *x, int64_t u) {
+  if (DT == ADC_F32) return Loader<ADC_F32>::template load8<false>(x, u * 8);
+  return Loader<ADC_F16>::template load8<false>(x, u * 8);  // raw 16-bit words
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// |f16| -> f64 straight from the packed half (F2F.F64.F16), added in order.
+__device__ __forceinline__ double f_h_f64(uint32_t h16) {
+  double r;
+  asm("cvt.f64.f16 %0, %1;" : "=d"(r) : "h"(static_cast<unsigned short>(h16)));
+  return r;
+}
+__device__ __forceinline__ void acc8(double *acc, uint4 h) {
+  const uint32_t w[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    acc[2 * j] = __dadd_rn(acc[2 * j], fabs(f_h_f64(w[j] & 0xffffu)));
+    acc[2 * j + 1] = __dadd_rn(acc[2 * j + 1], fabs(f_h_f64(w[j] >> 16)));
+  }
+}
+
+// Units of 8 elements, fetched from the resident tile (after its bulk copy
+// landed) or from global memory.
+template <int DT>
+struct FSrc {
+  const unsigned char *tile;
+  const void *x;
+  int64_t u0, ures;
+  const uint64_t *bar;
+  __device__ __forceinline__ uint4 raw(int64_t u, int &waited) const {
+    if (u < ures) {
+      const int64_t off = (u - u0) * FTile<DT>::kUB;
+      const int ch = static_cast<int>(off / kFChunk);
+      if (ch != waited) {
+        mbar_wait(const_cast<uint64_t *>(bar + ch), 0);
+        waited = ch;
+      }
+      return FTile<DT>::raw(tile + off);
+    }
+    return f_global_raw<DT>(x, u);
+  }
+};
+
+// 16-bit raw words -> f16 words (bf16 inputs are rounded to f16 RNE first)
+template <int DT>
+__device__ __forceinline__ uint4 f_to_f16(uint4 v) {
+  if (DT == ADC_BF16) return make_uint4(bf2_to_h2(v.x), bf2_to_h2(v.y), bf2_to_h2(v.z), bf2_to_h2(v.w));
+  return v;
+}
+
+// Phase C (prediction missed): quantise the CTA's slice [u0, u1) again with
+// the actual flags.  Out of line: rare, and it keeps the hot code compact.
+template <int DT, int L>
+__device__ __noinline__ void requant_slice(FSrc<DT> src, const uint8_t *s_flag, int64_t u0, int64_t u1,
+                                           int cu, uint32_t *codes, uint16_t *scales, uint32_t *err) {
+  constexpr bool BF = DT == ADC_BF16;
+  const int tid = threadIdx.x;
+  int waited = -1;  // chunks completed in phase A; the re-checks return at once
+  const int step_cu = kFT % cu;
+  int ucol = static_cast<int>((u0 + tid) % cu);
+  const int64_t trips = (u1 - u0 + kFT - 1) / kFT;
+  for (int64_t i = 0; i < trips; i += 2) {
+    const int64_t ua = u0 + tid + i * kFT, ub = ua + kFT;
+    const bool aa = ua < u1, ab = ub < u1;
+    int ucol_b = ucol + step_cu;
+    if (ucol_b >= cu) ucol_b -= cu;
+    const uint4 va = aa ? src.raw(ua, waited) : make_uint4(0, 0, 0, 0);
+    const uint4 vb = ab ? src.raw(ub, waited) : make_uint4(0, 0, 0, 0);
+    uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+    zero_apply8(wa, *reinterpret_cast<const uint2 *>(s_flag + 8 * ucol));
+    zero_apply8(wb, *reinterpret_cast<const uint2 *>(s_flag + 8 * ucol_b));
+    uint16_t sa, sb;
+    bool bada, badb;
+    const uint32_t ca = sym_unit8<BF, L>(wa, aa, sa, bada);
+    const uint32_t cb = sym_unit8<BF, L>(wb, ab, sb, badb);
+    if (aa) {
+      codes[ua] = ca;
+      if ((ua & (L - 1)) == 0) {
+        scales[ua / L] = sa;
+        if (bada) raise_err(err, ADC_ERR_NONFINITE);
+      }
+    }
+    if (ab) {
+      codes[ub] = cb;
+      if ((ub & (L - 1)) == 0) {
+        scales[ub / L] = sb;
+        if (badb) raise_err(err, ADC_ERR_NONFINITE);
+      }
+    }
+    ucol = ucol_b + step_cu;
+    if (ucol >= cu) ucol -= cu;
+  }
+}
+
+template <int DT, int L>
+__global__ void __launch_bounds__(kFT, 1) outlier_fused(FusedArgs a) {
+  extern __shared__ __align__(128) unsigned char f_smem[];
+  __shared__ __align__(8) uint64_t s_bar[kFMaxChunks];
+  __shared__ int s_last;
+  __shared__ __align__(8) uint64_t s_sbar;  // bulk copy of the column sums
+  using T = FTile<DT>;
+  constexpr int UB = T::kUB;
+  constexpr bool BF = DT == ADC_BF16;
+  const int tid = threadIdx.x;
+  const int64_t P = gridDim.x, b = blockIdx.x;
+  const int64_t cols = a.cols, rows = a.rows;
+  const long long t_0 = clock64();
+  if (a.trace && tid == 0 && b < kTraceCtas) {
+    unsigned long long gt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+    g_ftrace[b * kTraceSlots] = gt;
+  }
+
+  // shared-memory carve-up (host computes the same sizes)
+  unsigned char *tile = f_smem;
+  double *red = reinterpret_cast<double *>(f_smem + a.tile_bytes);           // kFT*8 doubles
+  unsigned char *scratch = reinterpret_cast<unsigned char *>(red + kFT * 8);  // stats scratch
+  uint8_t *s_flag = scratch + ((kStatsScratch + 15) & ~15);                    // cols + 8
+  uint8_t *s_pflag = s_flag + ((cols + 8 + 15) & ~15);                         // cols + 8
+  uint32_t *s_idx = reinterpret_cast<uint32_t *>(s_pflag + ((cols + 8 + 15) & ~15));
+
+  // this CTA's slice: whole groups [g0, g1) -> units [u0, u1)
+  const int64_t g0 = a.n_groups * b / P, g1 = a.n_groups * (b + 1) / P;
+  const int64_t u0 = g0 * L, u1 = g1 * L;
+  // resident units: the whole slice if it fits, else whole phase-A trips
+  const int64_t nres = (u1 - u0 <= a.res_units) ? u1 - u0 : a.res_units / a.stride * a.stride;
+  const int64_t ures = u0 + nres;  // units [u0, ures) are resident
+  const int64_t res_bytes = nres * UB;
+  const int nch = static_cast<int>((res_bytes + kFChunk - 1) / kFChunk);
+
+  if (tid == 0) {
+    for (int c = 0; c < nch; ++c) mbar_init(&s_bar[c], 1);
+    mbar_init(&s_sbar, 1);
+    fence_barrier_init();
+    const char *src = static_cast<const char *>(a.x) + u0 * UB;
+    for (int c = 0; c < nch; ++c) {
+      const int64_t off = static_cast<int64_t>(c) * kFChunk;
+      const uint32_t bytes = static_cast<uint32_t>(min(static_cast<int64_t>(kFChunk), res_bytes - off));
+      mbar_expect_tx(&s_bar[c], bytes);
+      bulk_g2s(tile + off, src + off, bytes, &s_bar[c]);
+    }
+  }
+  __shared__ PwTree s_tree;
+  if (tid == 0) s_tree = a.tree;
+  // the predicted channel set (previous call's flags), 8 columns per thread:
+  // fetched now, parked in shared memory after phase A
+  const uint2 pf_pre = (a.spec && 8 * tid < cols) ? *reinterpret_cast<const uint2 *>(a.pflag + 8 * tid)
+                                                  : make_uint2(0, 0);
+  __syncthreads();
+  const FSrc<DT> src{tile, a.x, u0, ures, s_bar};
+
+  // ---- A: column |x| sums.  Thread t owns column unit (u0 + t) % cu for
+  // all its units (slice-local unit loc = t + i * stride).  The resident
+  // part (trips [0, nr / stride); the host makes nr a multiple of stride) is
+  // only summed here -- it is quantised below while warp 0 waits at the grid
+  // barrier; the streamed rest is summed AND speculatively quantised with the
+  // predicted flags while it is in registers, one step prefetched.
+  const int cu = a.cu, stride = a.stride;
+  const bool lane_on = tid < stride;
+  const int nslice = static_cast<int>(u1 - u0), nr = static_cast<int>(nres);
+  uint32_t *codes = a.codes + u0;
+  uint16_t *scales = a.scales + u0 / L;
+  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if ((tid & ~31) < stride) {  // warps with at least one owner lane (uniform trip count)
+    const int trips = (nslice + stride - 1) / stride;
+    const int tr_res = (nr + stride - 1) / stride;
+    const int ucol = static_cast<int>((u0 + tid) % cu);
+    int waited = -1;
+    auto res_unit = [&](int loc) -> uint4 {
+      if (!lane_on || loc >= nr) return make_uint4(0, 0, 0, 0);
+      const int ch = (loc * UB) / kFChunk;
+      if (ch != waited) {
+        mbar_wait(&s_bar[ch], 0);
+        waited = ch;
+      }
+      return T::raw(tile + loc * UB);
+    };
+    for (int i = 0; i < tr_res; i += 2) {  // two units in flight
+      const uint4 va = res_unit(tid + i * stride);
+      const uint4 vb = (i + 1 < tr_res) ? res_unit(tid + (i + 1) * stride) : make_uint4(0, 0, 0, 0);
+      acc8(acc, f_to_f16<DT>(va));
+      acc8(acc, f_to_f16<DT>(vb));
+    }
+    if (tr_res < trips) {
+      // the thread's column is fixed: the predicted zeroing is four AND masks
+      uint32_t mk[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
+      if (a.spec && lane_on) zero_apply8(mk, *reinterpret_cast<const uint2 *>(a.pflag + 8 * ucol));
+      const char *xg = static_cast<const char *>(a.x) + u0 * UB;
+      auto gload = [&](int loc) -> uint4 {
+        if (!lane_on || loc >= nslice) return make_uint4(0, 0, 0, 0);
+        if (DT == ADC_F32) return Loader<ADC_F32>::template load8<false>(xg, static_cast<int64_t>(loc) * 8);
+        return ld_stream16(xg + static_cast<int64_t>(loc) * UB);
+      };
+      int la = tid + tr_res * stride;
+      uint4 na = gload(la), nb = gload(la + stride);
+      for (int i = tr_res; i < trips; i += 2, la += 2 * stride) {
+        const int lb = la + stride;
+        const uint4 va = na, vb = nb;
+        na = gload(la + 2 * stride);
+        nb = gload(lb + 2 * stride);
+        const bool aa = lane_on && la < nslice, ab = lane_on && lb < nslice;
+        acc8(acc, f_to_f16<DT>(va));
+        acc8(acc, f_to_f16<DT>(vb));
+        if (a.spec) {
+          uint32_t wa[4] = {va.x & mk[0], va.y & mk[1], va.z & mk[2], va.w & mk[3]};
+          uint32_t wb[4] = {vb.x & mk[0], vb.y & mk[1], vb.z & mk[2], vb.w & mk[3]};
+          uint16_t sa, sb;
+          bool bada, badb;
+          const uint32_t ca = sym_unit8<BF, L>(wa, aa, sa, bada);
+          const uint32_t cb = sym_unit8<BF, L>(wb, ab, sb, badb);
+          if (aa) {
+            codes[la] = ca;
+            if ((la & (L - 1)) == 0) {
+              scales[la / L] = sa;
+              if (bada) raise_err(a.err, ADC_ERR_NONFINITE);
+            }
+          }
+          if (ab) {
+            codes[lb] = cb;
+            if ((lb & (L - 1)) == 0) {
+              scales[lb / L] = sb;
+              if (badb) raise_err(a.err, ADC_ERR_NONFINITE);
+            }
+          }
+        }
+      }
+    }
+  }
+  FTRACE(1);
+  // the predicted channel set (previous call's flags) for the quantisation below
+  if (a.spec && 8 * tid < cols) *reinterpret_cast<uint2 *>(s_pflag + 8 * tid) = pf_pre;
+  // fold the row lanes; one reduction per column and CTA (red.global.add.f64)
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[tid * 8 + j] = acc[j];
+  __syncthreads();
+  {
+    const int lanes = stride / cu;
+    const int base = static_cast<int>(u0 % cu);  // thread t holds column unit (base + t) % cu
+    for (int c = tid; c < cols; c += kFT) {
+      const int unit = c >> 3, j = c & 7;
+      const int t0 = (unit - base + cu) % cu;
+      double v = 0.0;
+      for (int q = 0; q < lanes; ++q) v = __dadd_rn(v, red[(t0 + q * cu) * 8 + j]);
+      if (v != 0.0) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a.acc + c), "d"(v) : "memory");
+    }
+  }
+  __syncthreads();
+  FTRACE(2);
+
+  // ---- B: warps 0-3 cross the grid barrier (release-add arrival, acquire
+  // poll by thread 0), pull the column sums into shared memory with one bulk
+  // copy and evaluate mean / sigma; warps 4.. meanwhile quantise the resident
+  // part with the predicted flags.
+  constexpr int kStatWarps = 4;
+  double *S = red;  // reuse: cols <= kFT * 8
+  __shared__ double s_ms[3];
+  __shared__ double s_part[kStatWarps];
+  __shared__ int s_tmp[64];
+  __shared__ int s_big;
+  unsigned ticket = 0;
+  if (tid < 32 * kStatWarps) {
+    if (tid == 0) {
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.cnt) : "memory");
+      while (ld_acquire_u32(a.cnt) < P) {
+      }
+      FTRACE(3);
+      // the sums were written by other SMs' reductions: order them before the
+      // async-proxy read
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      mbar_expect_tx(&s_sbar, static_cast<uint32_t>(cols * 8));
+      bulk_g2s(S, a.acc, static_cast<uint32_t>(cols * 8), &s_sbar);
+    }
+    mbar_wait(&s_sbar, 0);
+    int big = 0;
+    for (int c = tid; c < cols; c += 32 * kStatWarps) {
+      const double v = S[c];
+      big |= (v >= kFExact) && (v <= 65504.0 * static_cast<double>(rows));  // finite but inexact
+    }
+    big = __any_sync(0xffffffffu, big);
+    if ((tid & 31) == 0) s_tmp[tid >> 5] = big;
+    named_bar(1, 32 * kStatWarps);
+    big = s_tmp[0] | s_tmp[1] | s_tmp[2] | s_tmp[3];
+    // departure ticket; its value is only needed after the statistics
+    if (tid == 0) ticket = atomicAdd(a.cnt + 1, 1u);
+    FTRACE(4);
+    if (!big) {
+      double mean, var;
+      group_mean_var<kStatWarps>(S, static_cast<int>(cols), s_tree, reinterpret_cast<double *>(scratch),
+                                 s_part, 1, mean, var);
+      const double sigma = __dsqrt_rn(var);
+      if (tid == 0) {
+        s_ms[0] = mean;
+        s_ms[1] = sigma;
+        s_ms[2] = sigma != 0.0 ? __drcp_rn(sigma) : 0.0;
+      }
+    }
+    if (tid == 0) s_big = big;
+    FTRACE(10);
+  } else if (a.spec && nr > 0) {
+    constexpr int NQ = kFT - 32 * kStatWarps;
+    const int tq = tid - 32 * kStatWarps;
+    const int step_cu = (2 * NQ) % cu;
+    int ucol_a = static_cast<int>((u0 + tq) % cu), ucol_b = static_cast<int>((u0 + tq + NQ) % cu);
+    const int trips = (nr + NQ - 1) / NQ;
+    for (int i = 0; i < trips; i += 2) {  // two units per lane in flight
+      const int la = tq + i * NQ, lb = la + NQ;
+      const bool aa = la < nr, ab = lb < nr;
+      const uint4 va = aa ? T::raw(tile + la * UB) : make_uint4(0, 0, 0, 0);
+      const uint4 vb = ab ? T::raw(tile + lb * UB) : make_uint4(0, 0, 0, 0);
+      uint32_t wa[4] = {va.x, va.y, va.z, va.w}, wb[4] = {vb.x, vb.y, vb.z, vb.w};
+      zero_apply8(wa, *reinterpret_cast<const uint2 *>(s_pflag + 8 * ucol_a));
+      zero_apply8(wb, *reinterpret_cast<const uint2 *>(s_pflag + 8 * ucol_b));
+      uint16_t sa, sb;
+      bool bada, badb;
+      const uint32_t ca = sym_unit8<BF, L>(wa, aa, sa, bada);
+      const uint32_t cb = sym_unit8<BF, L>(wb, ab, sb, badb);
+      if (aa) {
+        codes[la] = ca;
+        if ((la & (L - 1)) == 0) {
+          scales[la / L] = sa;
+          if (bada) raise_err(a.err, ADC_ERR_NONFINITE);
+        }
+      }
+      if (ab) {
+        codes[lb] = cb;
+        if ((lb & (L - 1)) == 0) {
+          scales[lb / L] = sb;
+          if (badb) raise_err(a.err, ADC_ERR_NONFINITE);
+        }
+      }
+      ucol_a += step_cu;
+      if (ucol_a >= cu) ucol_a -= cu;
+      ucol_b += step_cu;
+      if (ucol_b >= cu) ucol_b -= cu;
+    }
+    FTRACE_BY(11, 32 * kStatWarps);
+    FTRACE_BY(12, kFT - 1);
+  }
+  __syncthreads();
+  if (s_big) {  // some column total >= 2^29: numpy's row order (rare; all CTAs)
+    for (int c = tid; c < cols; c += kFT) {
+      double sum = 0.0;
+      for (int64_t r = 0; r < rows; ++r)
+        sum = __dadd_rn(sum, fabs(static_cast<double>(h2f(Loader<DT>::load1(a.x, r * cols + c)))));
+      S[c] = sum;
+    }
+    __syncthreads();
+    if (tid < 32 * kStatWarps) {
+      double mean, var;
+      group_mean_var<kStatWarps>(S, static_cast<int>(cols), s_tree, reinterpret_cast<double *>(scratch),
+                                 s_part, 1, mean, var);
+      const double sigma = __dsqrt_rn(var);
+      if (tid == 0) {
+        s_ms[0] = mean;
+        s_ms[1] = sigma;
+        s_ms[2] = sigma != 0.0 ? __drcp_rn(sigma) : 0.0;
+      }
+    }
+    __syncthreads();
+  }
+  FTRACE(8);
+  const int k = outlier_flags_fast(S, rows, static_cast<int>(cols), s_ms[0], s_ms[1], s_ms[2], a.thr,
+                                   a.kidx_cap, s_flag, s_idx, b == 0 ? a.k_out : nullptr,
+                                   b == 0 ? a.err : nullptr, s_tmp);
+  __syncthreads();
+  FTRACE(9);
+  if (tid == 0) s_last = ticket == P - 1;
+  // prediction check (all CTAs reach the same verdict)
+  int miss = !a.spec;
+  if (a.spec)
+    for (int c = tid; c < cols; c += kFT) miss |= s_flag[c] != s_pflag[c];
+  miss = __syncthreads_or(miss);
+  FTRACE(5);
+  if (s_last) {  // every CTA has read the sums: clean up for the next call
+    for (int c = tid; c < cols; c += kFT) __stcg(a.acc + c, 0.0);
+    if (tid == 0) {
+      a.cnt[0] = 0;
+      a.cnt[1] = 0;
+    }
+  }
+  const int kk = min(k, a.kidx_cap);
+  if (b == 0) {
+    for (int i = tid; i < kk; i += kFT) a.idx[i] = s_idx[i];
+    if (miss && a.spec)
+      for (int c = tid; c < cols; c += kFT) a.pflag[c] = s_flag[c];
+  }
+
+  // ---- C (prediction missed): quantise this slice with the actual flags
+  if (miss) requant_slice<DT, L>(src, s_flag, u0, u1, cu, a.codes, a.scales, a.err);
+  FTRACE(6);
+  // side buffer: val[j][r] = f16(x[r, idx[j]]) for the elements of this slice
+  if (kk > 0) {
+    const int64_t e0 = u0 * 8, e1 = u1 * 8;
+    const int64_t r_lo = e0 / cols, r_hi = (e1 - 1) / cols;
+    const int64_t items = (r_hi - r_lo + 1) * kk;
+    for (int64_t it = tid; it < items; it += kFT) {
+      const int64_t j = it % kk, r = r_lo + it / kk;
+      const int64_t e = r * cols + s_idx[j];
+      if (e < e0 || e >= e1) continue;
+      const uint16_t h = e < ures * 8 ? T::one(tile + (e - e0) * (UB / 8)) : Loader<DT>::load1(a.x, e);
+      a.val[j * rows + r] = h;
+    }
+  }
+  FTRACE(7);
+}
+
+// ---------------------------------------------------------------------------
+static int optin_smem() {
+  static int v = 0;
+  if (!v) {
+    int dev = 0, s = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&s, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || s <= 0)
+      s = 227 * 1024;
+    v = s;
+  }
+  return v;
+}
+
+template <int DT, int L>
+static int fused_go(const Ctx &c, FusedArgs a, size_t other_smem, int64_t per_cta_units) {
+  auto kern = outlier_fused<DT, L>;
+  constexpr int UB = FTile<DT>::kUB;
+  const int static_smem = 1024;  // barriers, stats scratch indices (conservative)
+  int64_t budget = optin_smem() - static_smem - static_cast<int64_t>(other_smem);
+  budget = std::min<int64_t>(budget, static_cast<int64_t>(kFChunk) * kFMaxChunks);
+  if (budget < 0) return 0;
+  const int64_t want = per_cta_units * UB;
+  int64_t tile = std::min<int64_t>(want, budget / UB * UB);
+  tile = (tile + 127) / 128 * 128;
+  if (tile > budget) tile -= 128;
+  if (tile < 0) tile = 0;
+  a.tile_bytes = static_cast<int>(tile);
+  a.res_units = static_cast<int>(tile / UB);
+  const size_t smem = static_cast<size_t>(tile) + other_smem;
+  static size_t configured = 0;
+  if (smem > configured) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    configured = smem;
+  }
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kFT, smem) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(c.num_sms));  // one CTA per SM: all co-resident
+  cfg.blockDim = dim3(kFT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = c.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  note_launches(1);
+  return 1;
+}
+
+// numpy's pairwise recursion (split n > 128 at n/2 - (n/2) % 8) flattened for
+// warp_tree_sum: leaves left to right, internal nodes ordered by height.
+static bool build_pw_tree(int n, PwTree &t) {
+  struct Internal { int l, r, h; };
+  std::vector<Internal> in;
+  std::vector<std::pair<int, int>> leaves;
+  // returns (encoded id, height); leaves encoded >= 0, internal as -(k + 1)
+  std::function<std::pair<int, int>(int, int)> rec = [&](int lo, int m) -> std::pair<int, int> {
+    if (m <= 128) {
+      leaves.emplace_back(lo, m);
+      return {static_cast<int>(leaves.size()) - 1, 0};
+    }
+    const int h = m / 2 - (m / 2) % 8;
+    const auto a = rec(lo, h), b = rec(lo + h, m - h);
+    in.push_back({a.first, b.first, 1 + std::max(a.second, b.second)});
+    return {-static_cast<int>(in.size()), in.back().h};
+  };
+  rec(0, n);
+  const int nl = static_cast<int>(leaves.size()), ni = static_cast<int>(in.size());
+  if (nl > kPwMaxLeaves || ni >= kPwMaxLeaves) return false;
+  std::vector<int> order(ni), pos(ni);
+  for (int i = 0; i < ni; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return in[x].h < in[y].h; });
+  for (int i = 0; i < ni; ++i) pos[order[i]] = i;
+  auto id = [&](int enc) { return enc >= 0 ? enc : nl + pos[-enc - 1]; };
+  t = PwTree{};
+  t.n_leaves = nl;
+  for (int i = 0; i < nl; ++i) {
+    t.leaf_lo[i] = static_cast<int16_t>(leaves[i].first);
+    t.leaf_n[i] = static_cast<int16_t>(leaves[i].second);
+  }
+  int levels = 0;
+  for (int j = 0; j < ni; ++j) {
+    const Internal &v = in[order[j]];
+    t.left[j] = static_cast<uint8_t>(id(v.l));
+    t.right[j] = static_cast<uint8_t>(id(v.r));
+    levels = std::max(levels, v.h);
+    t.level_end[v.h - 1] = static_cast<uint8_t>(j + 1);
+  }
+  t.n_levels = levels;
+  return levels <= 8;
+}
+
+static std::atomic<int> g_trace{0};
+void set_fused_trace(int v) { g_trace.store(v, std::memory_order_relaxed); }
+int read_fused_trace(unsigned long long *host, int n) {
+  if (n > kTraceCtas * kTraceSlots) n = kTraceCtas * kTraceSlots;
+  return cudaMemcpyFromSymbol(host, g_ftrace, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
+}
+
+static std::atomic<int> g_fused{-1};
+bool use_fused_outlier() {
+  int v = g_fused.load(std::memory_order_relaxed);
+  if (v < 0) {
+    // measured (B200, bf16 [8192,1024] / [8192,4096], predictions hitting):
+    // 20.9 / 56.7 us fused vs 19.9 / 51.9 us for the two launches, so the
+    // two-launch path stays the default; ADC_OUTLIER_PATH=1 selects this one
+    const char *e = getenv("ADC_OUTLIER_PATH");
+    v = (e && e[0] == '1') ? 1 : 0;
+    g_fused.store(v, std::memory_order_relaxed);
+  }
+  return v == 1;
+}
+void set_fused_outlier(int v) { g_fused.store(v ? 1 : 0, std::memory_order_relaxed); }
+
+int launch_outlier_fused(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                         int64_t g, double thr, int64_t k_cap, const Workspace &ws,
+                         uint8_t *codes, uint16_t *scales, uint32_t *idx, uint16_t *val,
+                         int32_t *k_out, uint32_t *err) {
+  if (!use_fused_outlier()) return 0;
+  const int64_t n = rows * cols;
+  if (cols % 8 || cols > kFMaxCols || g < 8 || g % 8 || n % g || n >= (1ll << 31)) return 0;
+  const int64_t L = g / 8;
+  if (L > 32 || (L & (L - 1))) return 0;
+  if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(codes) % 4) return 0;
+  if (k_cap > 0 && (!idx || !val)) return 0;
+  if (dt != ADC_BF16 && dt != ADC_F16 && dt != ADC_F32) return 0;
+  FusedArgs a{};
+  a.x = x;
+  a.rows = rows;
+  a.cols = cols;
+  a.n_groups = n / g;
+  a.cu = static_cast<int>(cols / 8);
+  a.stride = (kFT / a.cu) * a.cu;
+  a.kidx_cap = static_cast<int>(std::min<int64_t>(std::max<int64_t>(k_cap, 0), cols));
+  a.thr = thr;
+  a.k_cap = k_cap;
+  a.acc = ws.acc;
+  a.cnt = ws.counters + 1;
+  a.codes = reinterpret_cast<uint32_t *>(codes);
+  a.scales = scales;
+  a.idx = idx;
+  a.val = val;
+  a.k_out = k_out;
+  a.err = err;
+  a.trace = g_trace.load(std::memory_order_relaxed);
+  a.pflag = ws.pflag;
+  {
+    static thread_local int tree_cols = -1;
+    static thread_local PwTree tree;
+    if (tree_cols != static_cast<int>(cols)) {
+      if (!build_pw_tree(static_cast<int>(cols), tree)) return 0;
+      tree_cols = static_cast<int>(cols);
+    }
+    a.tree = tree;
+  }
+  a.spec = (cols % g == 0) ? 1 : 0;
+  const size_t other = static_cast<size_t>(kFT) * 8 * sizeof(double) + ((kStatsScratch + 15) & ~15) +
+                       2 * ((cols + 8 + 15) & ~15) + static_cast<size_t>(a.kidx_cap) * 4 + 16;
+  const int64_t groups_per_cta = (a.n_groups + c.num_sms - 1) / c.num_sms;
+  const int64_t per_cta_units = groups_per_cta * L;
+#define ADC_FUSED_L(DTV)                                                             \
+  switch (L) {                                                                       \
+    case 1: return fused_go<DTV, 1>(c, a, other, per_cta_units);                     \
+    case 2: return fused_go<DTV, 2>(c, a, other, per_cta_units);                     \
+    case 4: return fused_go<DTV, 4>(c, a, other, per_cta_units);                     \
+    case 8: return fused_go<DTV, 8>(c, a, other, per_cta_units);                     \
+    case 16: return fused_go<DTV, 16>(c, a, other, per_cta_units);                   \
+    case 32: return fused_go<DTV, 32>(c, a, other, per_cta_units);                   \
+  }
+  switch (dt) {
+    case ADC_BF16: ADC_FUSED_L(ADC_BF16); break;
+    case ADC_F16: ADC_FUSED_L(ADC_F16); break;
+    case ADC_F32: ADC_FUSED_L(ADC_F32); break;
+  }
+#undef ADC_FUSED_L
+  return 0;
+}
+
+}  // namespace adc

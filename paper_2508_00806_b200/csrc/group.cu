@@ -14,24 +14,12 @@
 
 #include "common.cuh"
 #include "launch.h"
+#include "quant.cuh"
 
 namespace adc {
 
 __device__ __forceinline__ uint32_t fastdiv(uint32_t n, const FastDiv &f) {
   return static_cast<uint32_t>((static_cast<uint64_t>(n) * f.m) >> f.p);
-}
-
-template <int L>
-__device__ __forceinline__ uint32_t warp_max_u2(uint32_t v) {
-#pragma unroll
-  for (int o = 1; o < L; o <<= 1) v = __vmaxu2(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
-}
-template <int L>
-__device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
-#pragma unroll
-  for (int o = 1; o < L; o <<= 1) v = __vminu2(v, __shfl_xor_sync(0xffffffffu, v, o));
-  return v;
 }
 
 // Zero the flagged channels of 8 consecutive elements (one row segment,
@@ -47,18 +35,6 @@ __device__ __forceinline__ uint2 zero_flags8(int64_t e, const FastDiv &dc,
   const uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
   return __ldg(reinterpret_cast<const uint2 *>(zflag + c));
 }
-__device__ __forceinline__ void zero_apply8(uint32_t *w, uint2 f) {
-  if ((f.x | f.y) != 0) {
-    // byte j of f is 0/1: 16-bit lane j is kept iff its flag is 0
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t fw = i < 2 ? f.x : f.y;
-      const uint32_t lo = (fw >> (16 * (i & 1))) & 0xffu, hi = (fw >> (16 * (i & 1) + 8)) & 0xffu;
-      w[i] &= (lo ? 0xffff0000u : 0xffffffffu) & (hi ? 0x0000ffffu : 0xffffffffu);
-    }
-  }
-}
-
 // Side-buffer gather for the outlier-separated scheme (codec.py:331-341):
 // val[rank][r] = f16(x[r, idx[rank]]).  Run by the first n_gather CTAs of the
 // quantising launch, right after the column statistics, while x is still in
@@ -93,44 +69,6 @@ __device__ __forceinline__ void gather_side(const void *__restrict__ x, const Ou
   }
 }
 
-__device__ __forceinline__ float lo_f(uint32_t w) {
-  return __low2float(*reinterpret_cast<const __half2 *>(&w));
-}
-__device__ __forceinline__ float hi_f(uint32_t w) {
-  return __high2float(*reinterpret_cast<const __half2 *>(&w));
-}
-
-// Raw-word element access.  bf16 inputs are quantised NATIVELY: every bf16
-// value with |x| >= 2^-17 is exactly representable in f16 (8-bit vs 11-bit
-// mantissa), so f16(x) == x and the per-element f32->f16->f32 round trip of
-// codec.py:158 is skipped.  Only groups whose scale could be affected by the
-// subnormal f16 rounding of tiny values take the converting path (see
-// below); f16 inputs need no conversion at all; f32 inputs are converted to
-// f16 on load.
-template <int DT>
-struct Raw {  // f16 words (F16, F32-converted)
-  static constexpr bool kBf16 = false;
-  template <bool KEEP>
-  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
-    return Loader<DT>::template load8<KEEP>(x, i);
-  }
-  __device__ __forceinline__ static float lo(uint32_t w) { return lo_f(w); }
-  __device__ __forceinline__ static float hi(uint32_t w) { return hi_f(w); }
-};
-template <>
-struct Raw<ADC_BF16> {
-  static constexpr bool kBf16 = true;
-  template <bool KEEP>
-  __device__ __forceinline__ static uint4 load8(const void *x, int64_t i) {
-    return Loader<ADC_F16>::template load8<KEEP>(x, i);  // raw 16-bit words
-  }
-  __device__ __forceinline__ static float lo(uint32_t w) { return __uint_as_float(w << 16); }
-  __device__ __forceinline__ static float hi(uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
-};
-
-__device__ __forceinline__ uint32_t bf16_bits_to_f16_bits(uint32_t b) {
-  return __half_as_ushort(__float2half_rn(__uint_as_float(b << 16)));
-}
 __device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
   __nv_bfloat162 r = __hmax2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
   return *reinterpret_cast<uint32_t *>(&r);
@@ -138,24 +76,6 @@ __device__ __forceinline__ uint32_t bmax2_nan(uint32_t a, uint32_t b) {
 __device__ __forceinline__ uint32_t bmin2_nan(uint32_t a, uint32_t b) {
   __nv_bfloat162 r = __hmin2_nan(*reinterpret_cast<__nv_bfloat162 *>(&a), *reinterpret_cast<__nv_bfloat162 *>(&b));
   return *reinterpret_cast<uint32_t *>(&r);
-}
-
-// Exact (converting) element codes for one unit: h = f16(x), float64 quotient
-// as in codec.py:223-231.  Used for the rare groups / units the fast paths
-// cannot decide.
-template <bool BF16, int NW>
-__device__ __forceinline__ void unit_codes_exact(const uint32_t *w, float s, float o, bool asym,
-                                              uint32_t *t) {
-#pragma unroll
-  for (int i = 0; i < 2 * NW; ++i) {
-    const uint32_t raw = (w[i >> 1] >> (16 * (i & 1))) & 0xffffu;
-    const uint32_t hb = BF16 ? bf16_bits_to_f16_bits(raw) : raw;
-    const double h = static_cast<double>(h2f(hb));
-    const double sd = s == 0.f ? 1.0 : static_cast<double>(s);
-    double r = rint((asym ? h - static_cast<double>(o) : h) / sd);
-    r = fmin(fmax(r, -8.0), 7.0);
-    t[i] = 0x4B400008u + static_cast<uint32_t>(static_cast<int>(r));
-  }
 }
 
 // Exact asymmetric code of one element (h = its f16 value) for the elements

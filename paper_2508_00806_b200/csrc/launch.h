@@ -40,6 +40,8 @@ struct Workspace {
   double *acc;           // cols       f64 atomic column-sum accumulators (zero at rest)
   uint32_t *macc;        // cols       u32 atomic column-max accumulators (zero at rest)
   uint32_t *counters;    // 4          arrival counters (zero at rest)
+  uint8_t *pflag;        // cols + 8   previous outlier flags (fused kernel's prediction; any
+                         //            content is valid, zero-fill = "no outliers")
   int32_t *node_lo;      // pairwise-tree nodes (used when cols > 16384)
   int32_t *node_n;
   int32_t *node_left;
@@ -73,6 +75,19 @@ void set_compress_path(int v);
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                           uint16_t *outl_val);
+
+// single-launch outlier-separated compress (fused.cu): returns 1 if it ran,
+// 0 if the shape / device is not eligible (the caller then uses the
+// colreduce + group_quant_fast pair, which writes identical bytes).
+int launch_outlier_fused(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
+                         int64_t g, double thr, int64_t k_cap, const Workspace &ws,
+                         uint8_t *codes, uint16_t *scales, uint32_t *idx, uint16_t *val,
+                         int32_t *k_out, uint32_t *err);
+// ADC_OUTLIER_PATH=2 selects the two-launch path (A/B testing).
+bool use_fused_outlier();
+void set_fused_outlier(int v);
+void set_fused_trace(int v);
+int read_fused_trace(unsigned long long *host, int n);
 
 // per-channel kernels (channel.cu)
 bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,

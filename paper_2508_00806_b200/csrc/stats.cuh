@@ -170,6 +170,292 @@ __device__ __forceinline__ double heap_sum(const T &t, int n, int D, double *val
   return r;
 }
 
+// ---- one warp, host-built tree (fused.cu): numpy's pairwise recursion for a
+// fixed length n <= 4096 flattened into leaves (left to right) and internal
+// nodes sorted by height, so one warp evaluates it with no block barrier.
+constexpr int kPwMaxLeaves = 40;
+struct PwTree {
+  int n_leaves, n_levels;
+  int16_t leaf_lo[kPwMaxLeaves], leaf_n[kPwMaxLeaves];
+  uint8_t left[kPwMaxLeaves], right[kPwMaxLeaves];  // internal node j = id n_leaves + j
+  uint8_t level_end[8];                              // internal nodes of height <= h+1: [0, level_end[h])
+};
+
+// pairwise_sum of the terms of t by warp 0 (all 32 lanes call); val holds
+// >= 2 * kPwMaxLeaves doubles of shared memory.  Returns 0.0 + sum (as the
+// block version) to every lane.
+template <class T>
+__device__ __forceinline__ double warp_tree_sum(const T &t, const PwTree &tr, double *val) {
+  const int lane = threadIdx.x & 31, grp = lane >> 3;
+  for (int base = 0; base < tr.n_leaves; base += 4) {
+    const int i = base + grp;
+    const bool v = i < tr.n_leaves;
+    const double s = leaf_sum8(t, v ? tr.leaf_lo[i] : 0, v ? tr.leaf_n[i] : 0, v);
+    if (v && (lane & 7) == 0) val[i] = s;
+  }
+  __syncwarp();
+  int beg = 0;
+  for (int h = 0; h < tr.n_levels; ++h) {
+    const int end = tr.level_end[h];
+    for (int j = beg + lane; j < end; j += 32)
+      val[tr.n_leaves + j] = __dadd_rn(val[tr.left[j]], val[tr.right[j]]);
+    __syncwarp();
+    beg = end;
+  }
+  const double r = __dadd_rn(0.0, val[tr.n_leaves + beg - 1 < tr.n_leaves ? 0 : tr.n_leaves + beg - 1]);
+  __syncwarp();
+  return r;
+}
+
+// Same sum, lower latency: a lane evaluates all its leaves (g, g + 4, ...)
+// with their chains interleaved, so the float64 adds of different leaves
+// overlap; the tree itself (tr) should live in shared memory.
+constexpr int kPwPerGroup = (kPwMaxLeaves + 3) / 4;
+template <class T>
+__device__ __forceinline__ double warp_tree_sum_ilp(const T &t, const PwTree &tr, double *val) {
+  const int lane = threadIdx.x & 31, g = lane >> 3, j = lane & 7;
+  const int nl = tr.n_leaves;
+  const int per = (nl + 3) / 4;  // leaves per group, warp-uniform bound
+  int lo[kPwPerGroup], stop[kPwPerGroup];
+  double r[kPwPerGroup];
+#pragma unroll
+  for (int l = 0; l < kPwPerGroup; ++l) {
+    const bool v = g + 4 * l < nl;
+    const int m = v ? tr.leaf_n[g + 4 * l] : 0;
+    lo[l] = v ? tr.leaf_lo[g + 4 * l] : 0;
+    stop[l] = m - m % 8;
+    r[l] = 0.0;  // 0.0 + a[j] == a[j] for the non-negative terms here
+  }
+  // branch-free: every lane issues every load (clamped address), a skipped
+  // term adds 0.0, so all chains of a lane overlap
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+#pragma unroll
+    for (int l = 0; l < kPwPerGroup; ++l) {
+      if (l >= per) break;
+      const bool ok = 8 * i < stop[l];
+      const double v = t.map(t.load(ok ? lo[l] + 8 * i + j : 0));
+      r[l] = __dadd_rn(r[l], ok ? v : 0.0);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < kPwPerGroup; ++l) {
+    if (l >= per) break;
+    const double a = __dadd_rn(r[l], __shfl_down_sync(0xffffffffu, r[l], 1, 8));
+    const double b = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, 2, 8));
+    double c = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, 4, 8));
+    if (g + 4 * l < nl && j == 0) {
+      const int m = tr.leaf_n[g + 4 * l];
+      if (m < 8) c = 0.0;
+      for (int q = stop[l]; q < m; ++q) c = __dadd_rn(c, t.map(t.load(lo[l] + q)));
+      val[g + 4 * l] = c;
+    }
+  }
+  __syncwarp();
+  int beg = 0;
+  for (int h = 0; h < tr.n_levels; ++h) {
+    const int end = tr.level_end[h];
+    for (int q = beg + lane; q < end; q += 32) val[nl + q] = __dadd_rn(val[tr.left[q]], val[tr.right[q]]);
+    __syncwarp();
+    beg = end;
+  }
+  const double res = __dadd_rn(0.0, val[beg == 0 ? 0 : nl + beg - 1]);
+  __syncwarp();
+  return res;
+}
+
+// The same tree sum by the first W warps of the block (threads [0, 32W)),
+// synchronised by named barrier `bar` (not 0): 4W groups of 8 lanes share
+// the leaves, each group's leaves interleaved.
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+template <int W, class T>
+__device__ __noinline__ double group_tree_sum(const T &t, const PwTree &tr, double *val, int bar) {
+  constexpr int G = 4 * W;                          // 8-lane groups
+  constexpr int PER = (kPwMaxLeaves + G - 1) / G;   // leaves per group (max)
+  const int tid = threadIdx.x, g = tid >> 3, j = tid & 7;
+  const int nl = tr.n_leaves;
+  const int per = (nl + G - 1) / G;
+  int lo[PER], stop[PER];
+  double r[PER];
+#pragma unroll
+  for (int l = 0; l < PER; ++l) {
+    const bool v = g + G * l < nl;
+    const int m = v ? tr.leaf_n[g + G * l] : 0;
+    lo[l] = v ? tr.leaf_lo[g + G * l] : 0;
+    stop[l] = m - m % 8;
+    r[l] = 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+#pragma unroll
+    for (int l = 0; l < PER; ++l) {
+      if (l >= per) break;
+      const bool ok = 8 * i < stop[l];
+      const double v = t.map(t.load(ok ? lo[l] + 8 * i + j : 0));
+      r[l] = __dadd_rn(r[l], ok ? v : 0.0);
+    }
+  }
+#pragma unroll
+  for (int l = 0; l < PER; ++l) {
+    if (l >= per) break;
+    const double a = __dadd_rn(r[l], __shfl_down_sync(0xffffffffu, r[l], 1, 8));
+    const double b = __dadd_rn(a, __shfl_down_sync(0xffffffffu, a, 2, 8));
+    double c = __dadd_rn(b, __shfl_down_sync(0xffffffffu, b, 4, 8));
+    if (g + G * l < nl && j == 0) {
+      const int m = tr.leaf_n[g + G * l];
+      if (m < 8) c = 0.0;
+      for (int q = stop[l]; q < m; ++q) c = __dadd_rn(c, t.map(t.load(lo[l] + q)));
+      val[g + G * l] = c;
+    }
+  }
+  named_bar(bar, 32 * W);
+  int beg = 0;
+  for (int h = 0; h < tr.n_levels; ++h) {
+    const int end = tr.level_end[h];
+    for (int q = beg + tid; q < end; q += 32 * W) val[nl + q] = __dadd_rn(val[tr.left[q]], val[tr.right[q]]);
+    named_bar(bar, 32 * W);
+    beg = end;
+  }
+  const double res = __dadd_rn(0.0, val[beg == 0 ? 0 : nl + beg - 1]);
+  named_bar(bar, 32 * W);
+  return res;
+}
+
+// Mean / population variance by the first W warps (see warp_mean_var).
+template <int W>
+__device__ __noinline__ void group_mean_var(const double *S, int n, const PwTree &tr, double *val,
+                                               double *s_part, int bar, double &mean, double &var) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  double p0 = 0.0, p1 = 0.0;  // any order: exact below 2^29
+  int c = tid;
+  for (; c + 32 * W < n; c += 64 * W) {
+    p0 = __dadd_rn(p0, S[c]);
+    p1 = __dadd_rn(p1, S[c + 32 * W]);
+  }
+  if (c < n) p0 = __dadd_rn(p0, S[c]);
+  double part = __dadd_rn(p0, p1);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+  if (lane == 0) s_part[wid] = part;
+  named_bar(bar, 32 * W);
+  double total = 0.0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) total = __dadd_rn(total, s_part[w]);
+  Term<true> t{S, 0.0, false};
+  if (!(total < 536870912.0)) total = group_tree_sum<W>(t, tr, val, bar);
+  mean = __ddiv_rn(__dadd_rn(0.0, total), static_cast<double>(n));
+  t.mean = mean;
+  t.squared = true;
+  var = __ddiv_rn(group_tree_sum<W>(t, tr, val, bar), static_cast<double>(n));
+}
+
+// Mean and population variance of S[0, n) exactly as numpy (codec.py:299-301)
+// by warp 0.  When the any-order float64 total stays below 2^29 every partial
+// sum of the pairwise tree is exact (non-negative multiples of 2^-24 below
+// 2^29), so the tree equals this plain warp reduction; otherwise the tree
+// is evaluated.  The variance terms are rounded, so they always follow the
+// tree.
+__device__ __forceinline__ void warp_mean_var(const double *S, int n, const PwTree &tr, double *val,
+                                              double &mean, double &var) {
+  const int lane = threadIdx.x & 31;
+  double p0 = 0.0, p1 = 0.0, p2 = 0.0, p3 = 0.0;  // any order: exact below 2^29
+  int c = lane;
+  for (; c + 96 < n; c += 128) {
+    p0 = __dadd_rn(p0, S[c]);
+    p1 = __dadd_rn(p1, S[c + 32]);
+    p2 = __dadd_rn(p2, S[c + 64]);
+    p3 = __dadd_rn(p3, S[c + 96]);
+  }
+  for (; c < n; c += 32) p0 = __dadd_rn(p0, S[c]);
+  double part = __dadd_rn(__dadd_rn(p0, p1), __dadd_rn(p2, p3));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+  Term<true> t{S, 0.0, false};
+  const double total = part < 536870912.0 ? part : warp_tree_sum_ilp(t, tr, val);
+  mean = __ddiv_rn(__dadd_rn(0.0, total), static_cast<double>(n));
+  t.mean = mean;
+  t.squared = true;
+  var = __ddiv_rn(warp_tree_sum_ilp(t, tr, val), static_cast<double>(n));
+}
+
+// Flags / ranks / indices for cols <= 8 * blockDim.x with mean, sigma and
+// 1/sigma given (same decision rule as outlier_flags_block), one block
+// barrier.  s_tmp: 2 * 32 ints of shared memory.  The caller synchronises
+// before reading flag / idx.
+__device__ __forceinline__ int outlier_flags_fast(const double *S, int64_t rows, int cols,
+                                                  double mean, double sigma, double rsig,
+                                                  double thr, int64_t k_cap, uint8_t *flag,
+                                                  uint32_t *idx, int32_t *k_out, uint32_t *err,
+                                                  int *s_tmp) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int run = (cols + blockDim.x - 1) / blockDim.x;  // <= 8
+  const int c0 = min(cols, run * tid), c1 = min(cols, c0 + run);
+  const double cap = 65504.0 * static_cast<double>(rows);
+  uint32_t f8 = 0, amb = 0;
+  int bad = 0;
+  double v[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) v[q] = c0 + q < c1 ? S[c0 + q] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const double qa = __dmul_rn(__dsub_rn(v[q], mean), rsig);
+    const double margin = __dadd_rn(__dmul_rn(fabs(qa), 0x1p-46), 0x1p-1000);
+    const bool hi = qa > __dadd_rn(thr, margin), lo = qa < __dsub_rn(thr, margin);
+    const bool live = c0 + q < c1;
+    bad |= live && !(v[q] <= cap);
+    f8 |= (live && hi && sigma != 0.0 ? 1u : 0u) << q;
+    amb |= (live && !hi && !lo && sigma != 0.0 ? 1u : 0u) << q;
+  }
+  while (amb) {  // rare: within 2^-46 of the threshold (or NaN)
+    const int q = __ffs(amb) - 1;
+    amb &= amb - 1;
+    f8 |= (__ddiv_rn(__dsub_rn(v[q], mean), sigma) > thr ? 1u : 0u) << q;
+  }
+  // exclusive prefix of the per-thread counts: warp scan + one block barrier
+  const int mine = __popc(f8);
+  int incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  const int wbad = __any_sync(0xffffffffu, bad);
+  if (lane == 31) {
+    s_tmp[wid] = incl;
+    s_tmp[32 + wid] = wbad;
+  }
+  __syncthreads();
+  int before = 0, total = 0, anybad = 0;
+  for (int w = 0; w < nw; ++w) {
+    const int cw = s_tmp[w];
+    before += w < wid ? cw : 0;
+    total += cw;
+    anybad |= s_tmp[32 + w];
+  }
+  int pos = before + incl - mine;
+  uint32_t kept = f8;
+  for (uint32_t m = f8; m; m &= m - 1, ++pos) {
+    const int q = __ffs(m) - 1;
+    if (pos < k_cap) {
+      if (idx) idx[pos] = static_cast<uint32_t>(c0 + q);
+    } else {
+      kept &= ~(1u << q);
+    }
+  }
+  for (int c = c0; c < c1; ++c) flag[c] = static_cast<uint8_t>((kept >> (c - c0)) & 1u);
+  if (tid == 0) {
+    if (k_out) *k_out = total;
+    if (err) {
+      if (anybad) atomicOr(err, ADC_ERR_NONFINITE);
+      if (2 * static_cast<int64_t>(total) > cols) atomicOr(err, ADC_ERR_TOO_MANY_OUTLIERS);
+      if (total > k_cap) atomicOr(err, ADC_ERR_K_CAP);
+    }
+  }
+  return total;
+}
+
 // ---- large vectors: level-parallel tree with the node arrays in the workspace.
 struct Tree {
   int32_t *lo, *n, *left;
@@ -243,38 +529,18 @@ static __device__ double tree_sum(const T &t, const Tree &tr, int depth, const i
   return r;
 }
 
-// Stage C: mean / std / z-score flags / indices (codec.py:294-305, 324-341).
-// S is in shared memory (s_in_smem) or in global memory written by this CTA;
-// `scratch` is >= kStatsScratch bytes of shared memory.  Outputs: flag[c]
-// (0/1 bytes, global), the ascending indices idx[0 .. min(k, k_cap)), k and
-// the error bits.  Columns ranked >= k_cap stay in their groups (flag 0):
-// graceful overflow, reported by ADC_ERR_K_CAP.
-constexpr int kStatsScratch = kHeapNodes * 8 + 8;
+// The z-score flags, ranks and outputs of detect_outlier_channels /
+// compress_outlier_separated given mean and population variance of S
+// (codec.py:302-305, 321-341); all threads of the block call.
 template <bool SMEM>
-__device__ __forceinline__ void outlier_stats_block(const double *S, int64_t rows,
-                                           int64_t cols, double thr, int64_t k_cap,
-                                           const Tree &tr, uint8_t *flag, uint32_t *idx,
-                                           int32_t *k_out, uint32_t *err, bool too_many_check,
-                                           unsigned char *scratch) {
-  __shared__ int s_lvl[72];
+__device__ __forceinline__ int outlier_flags_block(Term<SMEM> t, double mean, double var,
+                                                   int64_t rows, int64_t cols, double thr,
+                                                   int64_t k_cap, uint8_t *flag, uint32_t *idx,
+                                                   int32_t *k_out, uint32_t *err,
+                                                   bool too_many_check) {
   __shared__ int s_tmp[32];
-  const int n = static_cast<int>(cols);
-  Term<SMEM> t{S, 0.0, false};
-  double mean, var;
-  if (cols <= kHeapMaxCols) {
-    double *val = reinterpret_cast<double *>(scratch);
-    const int D = heap_depth(n);
-    mean = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
-    t.mean = mean;
-    t.squared = true;
-    var = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
-  } else {
-    const int depth = build_tree(n, tr, s_lvl, s_tmp);
-    mean = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
-    t.mean = mean;
-    t.squared = true;
-    var = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
-  }
+  t.mean = mean;
+  t.squared = false;
   const double sigma = __dsqrt_rn(var);
   const double cap = 65504.0 * static_cast<double>(rows);
   // z-score flag (strict >, codec.py:305); a sum above rows * 65504 means an
@@ -367,6 +633,43 @@ __device__ __forceinline__ void outlier_stats_block(const double *S, int64_t row
       if (total > k_cap) atomicOr(err, ADC_ERR_K_CAP);
     }
   }
+  return total;
+}
+
+// Stage C: mean / std / z-score flags / indices (codec.py:294-305, 324-341).
+// S is in shared memory (s_in_smem) or in global memory written by this CTA;
+// `scratch` is >= kStatsScratch bytes of shared memory.  Outputs: flag[c]
+// (0/1 bytes, global), the ascending indices idx[0 .. min(k, k_cap)), k and
+// the error bits.  Columns ranked >= k_cap stay in their groups (flag 0):
+// graceful overflow, reported by ADC_ERR_K_CAP.  Returns k to every thread.
+constexpr int kStatsScratch = kHeapNodes * 8 + 8;
+template <bool SMEM>
+__device__ __forceinline__ int outlier_stats_block(const double *S, int64_t rows,
+                                           int64_t cols, double thr, int64_t k_cap,
+                                           const Tree &tr, uint8_t *flag, uint32_t *idx,
+                                           int32_t *k_out, uint32_t *err, bool too_many_check,
+                                           unsigned char *scratch) {
+  __shared__ int s_lvl[72];
+  __shared__ int s_tmp[32];
+  const int n = static_cast<int>(cols);
+  Term<SMEM> t{S, 0.0, false};
+  double mean, var;
+  if (cols <= kHeapMaxCols) {
+    double *val = reinterpret_cast<double *>(scratch);
+    const int D = heap_depth(n);
+    mean = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
+    t.mean = mean;
+    t.squared = true;
+    var = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
+  } else {
+    const int depth = build_tree(n, tr, s_lvl, s_tmp);
+    mean = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
+    t.mean = mean;
+    t.squared = true;
+    var = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
+  }
+  return outlier_flags_block(t, mean, var, rows, cols, thr, k_cap, flag, idx, k_out, err,
+                             too_many_check);
 }
 
 }  // namespace adc

@@ -318,3 +318,77 @@ def test_graph_replay_matches_eager(torch_cuda, scheme, group):
             for a, b in zip(got, want):
                 assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
     assert int(slot.status[0]) == 0
+
+
+@pytest.mark.parametrize("shape,dtype_name,group", [
+    ((8192, 1024), "bfloat16", 128), ((8192, 4096), "bfloat16", 128), ((8192, 768), "float32", 128),
+    ((4096, 4096), "float16", 128), ((333, 1024), "bfloat16", 64), ((1000, 40), "float32", 8),
+    ((64, 4096), "bfloat16", 256), ((16384, 1024), "bfloat16", 128), ((300, 8), "float16", 16)])
+def test_fused_outlier_matches_two_launch_path(torch_cuda, shape, dtype_name, group):
+    """The single-launch cooperative K4 (fused.cu) writes the same bytes as
+    colreduce + quantiser, and both match the oracle; it is one launch."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200 import _lib
+    rng = np.random.default_rng(shape[0] + 3 * shape[1] + group)
+    x = rng.normal(size=shape).astype(np.float32)
+    hot = rng.choice(shape[1], max(1, shape[1] // 50), replace=False)
+    x[:, hot] *= rng.uniform(8, 50)
+    xt = torch.from_numpy(x).to(getattr(torch, dtype_name)).cuda()
+    want = oracle_run(xt.cpu().to(torch.float32).numpy(), cases.OUTL, group, 3.0)
+    spec = adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED, group)
+    two = device_run(xt, cases.OUTL, group, 3.0)
+    try:
+        _lib.set_option("outlier_path", 1)
+        n0 = _lib.lib().adc_kernel_launches()
+        ct = adc.compress(xt, spec)
+        torch.cuda.synchronize()
+        assert _lib.lib().adc_kernel_launches() - n0 == 1
+        fused = device_run(xt, cases.OUTL, group, 3.0)
+    finally:
+        _lib.set_option("outlier_path", 2)
+    assert cases.norm_digest(*fused) == cases.norm_digest(*two) == cases.norm_digest(*want)
+    idx = want[0]["idx"]
+    assert ct.outlier_count == (0 if idx is None else len(idx))
+
+
+@pytest.mark.parametrize("dtype_name,cols", [("bfloat16", 1024), ("float32", 768), ("float16", 4096)])
+def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols):
+    """A slot's workspace carries the previous call's channel set; the fused
+    kernel quantises speculatively with it and re-quantises when the actual
+    set differs.  Alternate inputs with different / equal outlier sets
+    through ONE slot and check every call against the oracle."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200.slots import CodecSlot
+    rows = 2048
+    rng = np.random.default_rng(cols)
+    base = rng.normal(size=(rows, cols)).astype(np.float32)
+    sets = [rng.choice(cols, 12, replace=False), rng.choice(cols, 7, replace=False), np.array([], int)]
+    seq = [0, 0, 1, 1, 0, 2, 2, 1, 0]
+    dt = getattr(torch, dtype_name)
+    from paper_2508_00806_b200 import _lib
+    _lib.set_option("outlier_path", 1)
+    slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), dt, torch.float32, k_cap=64)
+    y = torch.empty(rows, cols, dtype=torch.float32, device="cuda")
+    for step, si in enumerate(seq):
+        x = base * rng.uniform(0.5, 2.0)
+        x[:, sets[si]] *= 40.0
+        xt = torch.from_numpy(x).to(dt).cuda()
+        sp = torch.cuda.current_stream().cuda_stream
+        slot.compress_ptr(xt.data_ptr(), sp)
+        slot.decompress_ptr(y.data_ptr(), sp)
+        torch.cuda.synchronize()
+        want, wdeq = oracle_run(xt.cpu().to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+        k = int(slot.k_status[1])
+        got = cases.normalized(slot.scales.cpu().numpy(), None, slot.codes.cpu().numpy(),
+                               slot.idx[:k].cpu().numpy(), slot.val[:k].cpu().numpy(), None)
+        for key in ("scales", "codes", "idx", "vals"):
+            w, g = want[key], got[key]
+            if w is None or w.size == 0:
+                assert g is None or g.size == 0, (step, key)
+            else:
+                np.testing.assert_array_equal(g, w, err_msg=f"step {step} {key}")
+        np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), wdeq.view(np.uint32))
+        assert int(slot.status[0]) == 0
+    _lib.set_option("outlier_path", 2)
