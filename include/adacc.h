@@ -89,6 +89,8 @@ ADC_API unsigned long long adc_kernel_launches(void);
 /*
  * Kernel-path selection (tuning / A-B testing; results are identical):
  *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
+ *   "epl"           32 (default) or 16 elements per lane in the group
+ *                   quantisers (also ADC_EPL=16).
  *   "outlier_path"  1 = single-launch cooperative outlier-separated compress
  *                   (where eligible), 2 = column-statistics launch + quantiser
  *                   launch (default: measured faster).  Also ADC_OUTLIER_PATH=1.

@@ -97,6 +97,10 @@ int adc_set_option(const char *key, int value) {
     set_compress_path(value);
     return ADC_OK;
   }
+  if (k == "epl") {  // elements per lane of the group quantiser: 32 (default) or 16
+    set_epl(value);
+    return ADC_OK;
+  }
   if (k == "trace") {  // record phase timestamps of the fused kernel (adc_debug_trace)
     set_fused_trace(value);
     return ADC_OK;

@@ -120,11 +120,14 @@ __device__ __forceinline__ uint32_t mux_word(const uint32_t *w, int j) {
   if (NW == 4) {
     const uint32_t a = selp_u32(j & 1, w[1], w[0]), b = selp_u32(j & 1, w[3], w[2]);
     return selp_u32(j & 2, b, a);
-  } else {
+  } else if (NW == 8) {
     const uint32_t a = selp_u32(j & 1, w[1], w[0]), b = selp_u32(j & 1, w[3], w[2]);
     const uint32_t c = selp_u32(j & 1, w[5 % NW], w[4 % NW]), d = selp_u32(j & 1, w[7 % NW], w[6 % NW]);
     const uint32_t ab = selp_u32(j & 2, b, a), cd = selp_u32(j & 2, d, c);
     return selp_u32(j & 4, cd, ab);
+  } else {
+    const uint32_t lo = mux_word<8>(w, j & 7), hi = mux_word<8>(w + (NW > 8 ? 8 : 0), j & 7);
+    return selp_u32(j & 8, hi, lo);
   }
 }
 
@@ -296,7 +299,9 @@ __global__ void __launch_bounds__(kThreads, 4)
       } else {  // bf16 group with a tiny maximum: exact converting path
         unit_codes_exact<BF, NW>(w[k], h2f(s_bits), 0.f, false, t);
       }
-      uint32_t c0 = pack8_tbits(t), c1 = NC == 2 ? pack8_tbits(t + 8) : 0u;
+      uint32_t cw[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) cw[q] = pack8_tbits(t + 8 * q);
       if (ASYM) {
         const float sc = h2f(s_bits), so = h2f(o_bits);
         const float scd = sc == 0.f ? 1.f : sc, inv = rcp_approx(scd);
@@ -312,17 +317,18 @@ __global__ void __launch_bounds__(kThreads, 4)
             const int code = asym_exact_code(h2f(BF ? bf16_bits_to_f16_bits(raw) : raw), scd, inv, so);
             const uint32_t sh = 4 * (i & 7), nib = static_cast<uint32_t>(code) & 0xfu;
             const uint32_t m = ~(0xfu << sh), v = nib << sh;
-            if (i < 8)
-              c0 = (c0 & m) | v;
-            else
-              c1 = (c1 & m) | v;
+#pragma unroll
+            for (int q = 0; q < NC; ++q)
+              if ((i >> 3) == q) cw[q] = (cw[q] & m) | v;
           }
         }
       }
       if (NC == 1) {
-        codes[u] = c0;
+        codes[u] = cw[0];
+      } else if (NC == 2) {
+        *reinterpret_cast<uint2 *>(codes + 2 * u) = make_uint2(cw[0], cw[NC - 1]);
       } else {
-        *reinterpret_cast<uint2 *>(codes + 2 * u) = make_uint2(c0, c1);
+        *reinterpret_cast<uint4 *>(codes + 4 * u) = make_uint4(cw[0], cw[1 % NC], cw[2 % NC], cw[3 % NC]);
       }
     }
   }
@@ -501,6 +507,21 @@ bool use_tma_compress() {
 
 void set_compress_path(int v) { g_compress_path.store(v ? 1 : 0, std::memory_order_relaxed); }
 
+// 32 elements per lane (one 128-bit code store, the group's scale work
+// amortised over twice the elements) vs 16; ADC_EPL=16 or
+// adc_set_option("epl", 16) selects the 16-element kernels (A/B testing).
+static std::atomic<int> g_epl{-1};
+bool use_epl32() {
+  int v = g_epl.load(std::memory_order_relaxed);
+  if (v < 0) {
+    const char *e = getenv("ADC_EPL");
+    v = (e && e[0] == '1') ? 16 : 32;
+    g_epl.store(v, std::memory_order_relaxed);
+  }
+  return v == 32;
+}
+void set_epl(int v) { g_epl.store(v == 16 ? 16 : 32, std::memory_order_relaxed); }
+
 static inline int grid_for(const Ctx &c, int64_t work_items, int per_block) {
   int64_t need = (work_items + per_block - 1) / per_block;
   int64_t cap = static_cast<int64_t>(c.num_sms) * 8;
@@ -567,6 +588,26 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
                                              scales, offsets, err);
     if (rc || !zero) return rc;
     return launch_outlier_gather(c, x, dt, idx, k_dev, k_cap, rows, cols, outl_val);
+  }
+  L = pc ? 0 : lanes_for_group(g, 32);
+  if (L > 0 && use_epl32() && n % 32 == 0 && aligned(x, 16) && aligned(codes, 16) && zero_ok) {
+    const int64_t n_units = n / 32;
+    const int64_t n_units_pad = (n_units + L - 1) / L * L;
+    const int grid = grid_for(c, n_units_pad, kThreads);
+    uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
+    ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
+      if (asym) {
+        group_quant_fast<DT, true, LL, false, 32, 1><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
+      } else if (zero) {
+        group_quant_fast<DT, false, LL, true, 32, 1><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
+      } else {
+        group_quant_fast<DT, false, LL, false, 32, 1><<<grid, kThreads, 0, c.stream>>>(
+            x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
+      }
+    }));
+    return 0;
   }
   L = pc ? 0 : lanes_for_group(g, 16);
   if (L > 0 && n % 16 == 0 && aligned(x, 16) && aligned(codes, 8) && zero_ok) {

@@ -71,6 +71,8 @@ int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows,
 // Tuning switch read once from the environment: ADC_COMPRESS_PATH=tma|regs (default regs).
 bool use_tma_compress();
 void set_compress_path(int v);
+bool use_epl32();
+void set_epl(int v);
 
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
