@@ -596,49 +596,6 @@ static int fused_go(const Ctx &c, FusedArgs a, size_t other_smem, int64_t per_ct
   return 1;
 }
 
-// numpy's pairwise recursion (split n > 128 at n/2 - (n/2) % 8) flattened for
-// warp_tree_sum: leaves left to right, internal nodes ordered by height.
-static bool build_pw_tree(int n, PwTree &t) {
-  struct Internal { int l, r, h; };
-  std::vector<Internal> in;
-  std::vector<std::pair<int, int>> leaves;
-  // returns (encoded id, height); leaves encoded >= 0, internal as -(k + 1)
-  std::function<std::pair<int, int>(int, int)> rec = [&](int lo, int m) -> std::pair<int, int> {
-    if (m <= 128) {
-      leaves.emplace_back(lo, m);
-      return {static_cast<int>(leaves.size()) - 1, 0};
-    }
-    const int h = m / 2 - (m / 2) % 8;
-    const auto a = rec(lo, h), b = rec(lo + h, m - h);
-    in.push_back({a.first, b.first, 1 + std::max(a.second, b.second)});
-    return {-static_cast<int>(in.size()), in.back().h};
-  };
-  rec(0, n);
-  const int nl = static_cast<int>(leaves.size()), ni = static_cast<int>(in.size());
-  if (nl > kPwMaxLeaves || ni >= kPwMaxLeaves) return false;
-  std::vector<int> order(ni), pos(ni);
-  for (int i = 0; i < ni; ++i) order[i] = i;
-  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return in[x].h < in[y].h; });
-  for (int i = 0; i < ni; ++i) pos[order[i]] = i;
-  auto id = [&](int enc) { return enc >= 0 ? enc : nl + pos[-enc - 1]; };
-  t = PwTree{};
-  t.n_leaves = nl;
-  for (int i = 0; i < nl; ++i) {
-    t.leaf_lo[i] = static_cast<int16_t>(leaves[i].first);
-    t.leaf_n[i] = static_cast<int16_t>(leaves[i].second);
-  }
-  int levels = 0;
-  for (int j = 0; j < ni; ++j) {
-    const Internal &v = in[order[j]];
-    t.left[j] = static_cast<uint8_t>(id(v.l));
-    t.right[j] = static_cast<uint8_t>(id(v.r));
-    levels = std::max(levels, v.h);
-    t.level_end[v.h - 1] = static_cast<uint8_t>(j + 1);
-  }
-  t.n_levels = levels;
-  return levels <= 8;
-}
-
 static std::atomic<int> g_trace{0};
 void set_fused_trace(int v) { g_trace.store(v, std::memory_order_relaxed); }
 int read_fused_trace(unsigned long long *host, int n) {

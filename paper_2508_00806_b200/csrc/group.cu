@@ -9,6 +9,7 @@
 // A group of g = 8*L elements is owned by L adjacent lanes of a warp and
 // reduced with L-wide xor shuffles; every lane derives the group's scale
 // itself (no broadcast), lane 0 of the group stores it.
+#include <algorithm>
 #include <atomic>
 #include <cstdlib>
 
@@ -482,11 +483,14 @@ __global__ void __launch_bounds__(kThreads)
     outlier_scatter(const uint32_t *__restrict__ idx, const uint16_t *__restrict__ val,
                     const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                     void *__restrict__ y) {
+  // blockIdx.y walks the ranks, x the rows: no division, coalesced side-buffer reads
   const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
-  for (int64_t t = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; t < k * rows;
-       t += static_cast<int64_t>(gridDim.x) * kThreads) {
-    const int64_t i = t / rows, r = t - i * rows;
-    Storer<OT>::store1(y, r * cols + idx[i], h2f(val[t]));
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
+    const int64_t c = __ldg(idx + j);
+    const uint16_t *vj = val + j * rows;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * kThreads)
+      Storer<OT>::store1(y, r * cols + c, h2f(__ldg(vj + r)));
   }
 }
 
@@ -742,7 +746,10 @@ int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *va
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot) {
   if (k_cap <= 0) return 0;
-  const int grid = grid_for(c, k_cap * rows, kThreads);
+  // ~4 rows per thread, ranks across grid.y (at most ~4 waves of CTAs)
+  const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((rows + 4 * kThreads - 1) / (4 * kThreads), 64));
+  const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(k_cap, std::max<int64_t>(1, 8 * c.num_sms / gx)));
+  const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(std::min<int64_t>(gy, 65535)));
   ADC_OT_SWITCH(ot, OT, outlier_scatter<OT><<<grid, kThreads, 0, c.stream>>>(
                             idx, val, k_dev, k_cap, rows, cols, y), note_launches(1));
   return 0;

@@ -4,6 +4,11 @@
 // See outlier.cu for the exactness argument.
 #pragma once
 
+#include <algorithm>
+#include <functional>
+#include <utility>
+#include <vector>
+
 #include "common.cuh"
 
 namespace adc {
@@ -180,6 +185,49 @@ struct PwTree {
   uint8_t left[kPwMaxLeaves], right[kPwMaxLeaves];  // internal node j = id n_leaves + j
   uint8_t level_end[8];                              // internal nodes of height <= h+1: [0, level_end[h])
 };
+
+// numpy's pairwise recursion (split n > 128 at n/2 - (n/2) % 8) flattened for
+// warp_tree_sum: leaves left to right, internal nodes ordered by height.
+inline bool build_pw_tree(int n, PwTree &t) {
+  struct Internal { int l, r, h; };
+  std::vector<Internal> in;
+  std::vector<std::pair<int, int>> leaves;
+  // returns (encoded id, height); leaves encoded >= 0, internal as -(k + 1)
+  std::function<std::pair<int, int>(int, int)> rec = [&](int lo, int m) -> std::pair<int, int> {
+    if (m <= 128) {
+      leaves.emplace_back(lo, m);
+      return {static_cast<int>(leaves.size()) - 1, 0};
+    }
+    const int h = m / 2 - (m / 2) % 8;
+    const auto a = rec(lo, h), b = rec(lo + h, m - h);
+    in.push_back({a.first, b.first, 1 + std::max(a.second, b.second)});
+    return {-static_cast<int>(in.size()), in.back().h};
+  };
+  rec(0, n);
+  const int nl = static_cast<int>(leaves.size()), ni = static_cast<int>(in.size());
+  if (nl > kPwMaxLeaves || ni >= kPwMaxLeaves) return false;
+  std::vector<int> order(ni), pos(ni);
+  for (int i = 0; i < ni; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return in[x].h < in[y].h; });
+  for (int i = 0; i < ni; ++i) pos[order[i]] = i;
+  auto id = [&](int enc) { return enc >= 0 ? enc : nl + pos[-enc - 1]; };
+  t = PwTree{};
+  t.n_leaves = nl;
+  for (int i = 0; i < nl; ++i) {
+    t.leaf_lo[i] = static_cast<int16_t>(leaves[i].first);
+    t.leaf_n[i] = static_cast<int16_t>(leaves[i].second);
+  }
+  int levels = 0;
+  for (int j = 0; j < ni; ++j) {
+    const Internal &v = in[order[j]];
+    t.left[j] = static_cast<uint8_t>(id(v.l));
+    t.right[j] = static_cast<uint8_t>(id(v.r));
+    levels = std::max(levels, v.h);
+    t.level_end[v.h - 1] = static_cast<uint8_t>(j + 1);
+  }
+  t.n_levels = levels;
+  return levels <= 8;
+}
 
 // pairwise_sum of the terms of t by warp 0 (all 32 lanes call); val holds
 // >= 2 * kPwMaxLeaves doubles of shared memory.  Returns 0.0 + sum (as the
@@ -388,30 +436,34 @@ __device__ __forceinline__ int outlier_flags_fast(const double *S, int64_t rows,
                                                   double mean, double sigma, double rsig,
                                                   double thr, int64_t k_cap, uint8_t *flag,
                                                   uint32_t *idx, int32_t *k_out, uint32_t *err,
-                                                  int *s_tmp) {
+                                                  int *s_tmp, bool too_many_check = true) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const int run = (cols + blockDim.x - 1) / blockDim.x;  // <= 8
+  const int run = (cols + blockDim.x - 1) / blockDim.x;  // <= 32
   const int c0 = min(cols, run * tid), c1 = min(cols, c0 + run);
   const double cap = 65504.0 * static_cast<double>(rows);
-  uint32_t f8 = 0, amb = 0;
+  uint32_t f8 = 0;
   int bad = 0;
-  double v[8];
+  for (int base = c0; base < c1; base += 8) {
+    uint32_t fb = 0, amb = 0;
+    double v[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) v[q] = c0 + q < c1 ? S[c0 + q] : 0.0;
+    for (int q = 0; q < 8; ++q) v[q] = base + q < c1 ? S[base + q] : 0.0;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const double qa = __dmul_rn(__dsub_rn(v[q], mean), rsig);
-    const double margin = __dadd_rn(__dmul_rn(fabs(qa), 0x1p-46), 0x1p-1000);
-    const bool hi = qa > __dadd_rn(thr, margin), lo = qa < __dsub_rn(thr, margin);
-    const bool live = c0 + q < c1;
-    bad |= live && !(v[q] <= cap);
-    f8 |= (live && hi && sigma != 0.0 ? 1u : 0u) << q;
-    amb |= (live && !hi && !lo && sigma != 0.0 ? 1u : 0u) << q;
-  }
-  while (amb) {  // rare: within 2^-46 of the threshold (or NaN)
-    const int q = __ffs(amb) - 1;
-    amb &= amb - 1;
-    f8 |= (__ddiv_rn(__dsub_rn(v[q], mean), sigma) > thr ? 1u : 0u) << q;
+    for (int q = 0; q < 8; ++q) {
+      const double qa = __dmul_rn(__dsub_rn(v[q], mean), rsig);
+      const double margin = __dadd_rn(__dmul_rn(fabs(qa), 0x1p-46), 0x1p-1000);
+      const bool hi = qa > __dadd_rn(thr, margin), lo = qa < __dsub_rn(thr, margin);
+      const bool live = base + q < c1;
+      bad |= live && !(v[q] <= cap);
+      fb |= (live && hi && sigma != 0.0 ? 1u : 0u) << q;
+      amb |= (live && !hi && !lo && sigma != 0.0 ? 1u : 0u) << q;
+    }
+    while (amb) {  // rare: within 2^-46 of the threshold (or NaN)
+      const int q = __ffs(amb) - 1;
+      amb &= amb - 1;
+      fb |= (__ddiv_rn(__dsub_rn(v[q], mean), sigma) > thr ? 1u : 0u) << q;
+    }
+    f8 |= fb << (base - c0);
   }
   // exclusive prefix of the per-thread counts: warp scan + one block barrier
   const int mine = __popc(f8);
@@ -449,7 +501,7 @@ __device__ __forceinline__ int outlier_flags_fast(const double *S, int64_t rows,
     if (k_out) *k_out = total;
     if (err) {
       if (anybad) atomicOr(err, ADC_ERR_NONFINITE);
-      if (2 * static_cast<int64_t>(total) > cols) atomicOr(err, ADC_ERR_TOO_MANY_OUTLIERS);
+      if (too_many_check && 2 * static_cast<int64_t>(total) > cols) atomicOr(err, ADC_ERR_TOO_MANY_OUTLIERS);
       if (total > k_cap) atomicOr(err, ADC_ERR_K_CAP);
     }
   }
