@@ -136,7 +136,7 @@ __device__ __forceinline__ uint32_t mux_word(const uint32_t *w, int j) {
 // of g = EPL*L elements is owned by L adjacent lanes; U units per lane are
 // loaded before any is processed (memory-level parallelism).
 template <int DT, bool ASYM, int L, bool ZERO, int EPL, int U>
-__global__ void __launch_bounds__(kThreads, 4)
+__global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
     group_quant_fast(const void *__restrict__ x, int64_t n_units, int64_t n_units_pad, FastDiv dc,
                      const uint8_t *__restrict__ zflag, OutlierSide side,
                      uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
@@ -564,6 +564,7 @@ static inline int lanes_for_group(int64_t g, int epl) {
   }
 
 constexpr int kUnroll = 2;
+constexpr int kU32 = 1;  // units in flight per lane at 32 elements per lane
 
 // Gather work: (k_cap / 8) rank blocks x (rows / 256) row blocks, at most
 // one CTA per SM (the gather is latency-bound and short).
@@ -597,17 +598,17 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
   if (L > 0 && use_epl32() && n % 32 == 0 && aligned(x, 16) && aligned(codes, 16) && zero_ok) {
     const int64_t n_units = n / 32;
     const int64_t n_units_pad = (n_units + L - 1) / L * L;
-    const int grid = grid_for(c, n_units_pad, kThreads);
+    const int grid = grid_for(c, n_units_pad, kThreads * kU32);
     uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
-        group_quant_fast<DT, true, LL, false, 32, 1><<<grid, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, true, LL, false, 32, kU32><<<grid, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 32, 1><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, false, LL, true, 32, kU32><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
-        group_quant_fast<DT, false, LL, false, 32, 1><<<grid, kThreads, 0, c.stream>>>(
+        group_quant_fast<DT, false, LL, false, 32, kU32><<<grid, kThreads, 0, c.stream>>>(
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
