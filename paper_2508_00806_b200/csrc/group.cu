@@ -283,11 +283,19 @@ __global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
         }
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
+          // correctly rounded h/s two lanes per FMUL2 / FFMA2 (Markstein),
+          // RNE by the magic add, clip to 7 on the bit pattern
           const float sc = h2f(s_bits), inv = rcp_approx(sc);
+          const uint64_t inv2 = f2_pack(inv, inv), ns2 = f2_pack(-sc, -sc), mg2 = f2_pack(kMagic8, kMagic8);
 #pragma unroll
           for (int i = 0; i < NW; ++i) {
-            t[2 * i] = sym_tbits(R::lo(w[k][i]), sc, inv);
-            t[2 * i + 1] = sym_tbits(R::hi(w[k][i]), sc, inv);
+            const uint64_t h2 = f2_pack(R::lo(w[k][i]), R::hi(w[k][i]));
+            const uint64_t r0 = f2_mul(h2, inv2);
+            const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
+            float tl, th;
+            f2_unpack(f2_add(r1, mg2), tl, th);
+            t[2 * i] = min(__float_as_uint(tl), 0x4B40000Fu);
+            t[2 * i + 1] = min(__float_as_uint(th), 0x4B40000Fu);
           }
         } else {
           const float s0 = h2f(s_bits), sc = s0 == 0.f ? 1.f : s0, inv = rcp_approx(sc);
