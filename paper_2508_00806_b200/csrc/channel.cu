@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kThreads)
 
   // Per-column quantisation constants for this thread's 8 columns.
   float qs[8], qi[8];
+  bool fast = true;  // every column scale of this thread is a normal f16 (the packed path)
   {
     uint32_t sb[8];
 #pragma unroll
@@ -53,6 +54,7 @@ __global__ void __launch_bounds__(kThreads)
       QParams q = make_qparams(static_cast<uint16_t>(sb[j]), 0);
       qs[j] = q.s;
       qi[j] = q.inv;
+      fast &= (sb[j] & 0x7fffu) >= 0x0400u;
     }
     if (blockIdx.y == 0 && warp == 0 && tyl == 0 && col_live) {
       uint4 v = make_uint4(sb[0] | (sb[1] << 16), sb[2] | (sb[3] << 16), sb[4] | (sb[5] << 16),
@@ -74,7 +76,27 @@ __global__ void __launch_bounds__(kThreads)
     }
     // byte j = code(row r, col j) | code(row r+1, col j) << 4
     uint32_t lo = 0, hi = 0;
-    {
+    if (fast) {
+      // rows r and r+1 of column j share its scale: one FMUL2 / two FFMA2
+      // give both correctly rounded quotients, the magic add rounds them,
+      // one IMAD joins the two nibbles into the byte (see pack8_tbits)
+      const uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w}, wb[4] = {hb.x, hb.y, hb.z, hb.w};
+      const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
+      uint32_t by[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint32_t sh = (j & 1) * 16;
+        const uint64_t h2 = f2_pack(h2f((wa[j >> 1] >> sh) & 0xffffu), h2f((wb[j >> 1] >> sh) & 0xffffu));
+        const uint64_t inv2 = f2_pack(qi[j], qi[j]), ns2 = f2_pack(-qs[j], -qs[j]);
+        const uint64_t r0 = f2_mul(h2, inv2);
+        const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
+        float ta, tb;
+        f2_unpack(f2_add(r1, mg2), ta, tb);
+        by[j] = min(__float_as_uint(tb), 0x4B40000Fu) * 16u + min(__float_as_uint(ta), 0x4B40000Fu);
+      }
+      lo = __byte_perm(__byte_perm(by[0], by[1], 0x0040), __byte_perm(by[2], by[3], 0x0040), 0x5410) ^ 0x88888888u;
+      hi = __byte_perm(__byte_perm(by[4], by[5], 0x0040), __byte_perm(by[6], by[7], 0x0040), 0x5410) ^ 0x88888888u;
+    } else {
       uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w};
       uint32_t wb[4] = {hb.x, hb.y, hb.z, hb.w};
 #pragma unroll
