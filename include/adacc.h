@@ -89,6 +89,7 @@ ADC_API unsigned long long adc_kernel_launches(void);
 /*
  * Kernel-path selection (tuning / A-B testing; results are identical):
  *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
+ *   "pdl"           1 = launch with programmatic dependent launch (0 default).
  *   "epl"           32 (default) or 16 elements per lane in the group
  *                   quantisers (also ADC_EPL=16).
  *   "outlier_path"  1 = single-launch cooperative outlier-separated compress

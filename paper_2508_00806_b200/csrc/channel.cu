@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kThreads)
     channel_quant(const void *__restrict__ x, int64_t rows, int64_t cols,
                   const uint32_t *__restrict__ colmax, uint8_t *__restrict__ codes,
                   uint16_t *__restrict__ scales) {
+  pdl_entry();
   __shared__ uint32_t stage[kTileCols * kWordStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 7;         // column unit inside the tile
@@ -148,6 +149,7 @@ template <int OT>
 __global__ void __launch_bounds__(kThreads)
     channel_dequant(const uint8_t *__restrict__ codes, const uint16_t *__restrict__ scales,
                     int64_t rows, int64_t cols, void *__restrict__ y) {
+  pdl_entry();
   __shared__ uint32_t stage[kTileCols * kWordStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 7, tyl = lane >> 3;
@@ -216,7 +218,7 @@ int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, i
   dim3 gq(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
           static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
   ADC_DT_SWITCH(dt, DT, {
-    channel_quant<DT><<<gq, kThreads, 0, c.stream>>>(x, rows, cols, ws.colmax, codes, scales), note_launches(1);
+    launch_k(channel_quant<DT>, gq, kThreads, 0, c.stream, x, rows, cols, ws.colmax, codes, scales), note_launches(1);
   });
   return 0;
 }
@@ -226,9 +228,9 @@ int launch_channel_decompress(const Ctx &c, const uint8_t *codes, const uint16_t
   dim3 g(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
          static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
   switch (ot) {
-    case ADC_F32: channel_dequant<ADC_F32><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
-    case ADC_BF16: channel_dequant<ADC_BF16><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
-    case ADC_F16: channel_dequant<ADC_F16><<<g, kThreads, 0, c.stream>>>(codes, scales, rows, cols, y), note_launches(1); break;
+    case ADC_F32: launch_k(channel_dequant<ADC_F32>, g, kThreads, 0, c.stream, codes, scales, rows, cols, y), note_launches(1); break;
+    case ADC_BF16: launch_k(channel_dequant<ADC_BF16>, g, kThreads, 0, c.stream, codes, scales, rows, cols, y), note_launches(1); break;
+    case ADC_F16: launch_k(channel_dequant<ADC_F16>, g, kThreads, 0, c.stream, codes, scales, rows, cols, y), note_launches(1); break;
     default: return -1;
   }
   return 0;

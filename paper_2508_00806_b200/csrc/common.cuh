@@ -443,6 +443,17 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch (every kernel is launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, launch.h): wait until
+// the preceding grid in the stream has completed and its memory is visible,
+// and let the next grid be scheduled as soon as all of this grid's CTAs have
+// started -- its launch and prologue then overlap this grid's tail.  Both
+// are no-ops for a normal launch.
+__device__ __forceinline__ void pdl_entry() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void raise_err(uint32_t *err, uint32_t bit) {
   if (err) atomicOr(err, bit);
 }

@@ -226,6 +226,7 @@ __device__ __noinline__ void requant_slice(FSrc<DT> src, const uint8_t *s_flag, 
 
 template <int DT, int L>
 __global__ void __launch_bounds__(kFT, 1) outlier_fused(FusedArgs a) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char f_smem[];
   __shared__ __align__(8) uint64_t s_bar[kFMaxChunks];
   __shared__ int s_last;

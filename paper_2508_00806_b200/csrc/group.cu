@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
                      const uint8_t *__restrict__ zflag, OutlierSide side,
                      uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                      uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
+  pdl_entry();
   constexpr int NW = EPL / 2;  // 16-bit pairs per unit
   constexpr int NC = EPL / 8;  // packed code words per unit
   using R = Raw<DT>;
@@ -347,6 +348,7 @@ template <int OT, bool ASYM, int L, int EPL, int U>
 __global__ void __launch_bounds__(kThreads)
     group_dequant_fast(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
                        const uint16_t *__restrict__ offsets, int64_t n_units, void *__restrict__ y) {
+  pdl_entry();
   constexpr int NC = EPL / 8;
   const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
   for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units;
@@ -390,6 +392,7 @@ __global__ void __launch_bounds__(kThreads)
                         bool pc, int64_t rows, int64_t cols, const uint8_t *__restrict__ zflag,
                         uint16_t *__restrict__ scales, uint16_t *__restrict__ offsets,
                         uint32_t *__restrict__ err) {
+  pdl_entry();
   const int lane = threadIdx.x & 31;
   const int64_t warps = static_cast<int64_t>(gridDim.x) * (kThreads / 32);
   for (int64_t j = static_cast<int64_t>(blockIdx.x) * (kThreads / 32) + threadIdx.x / 32;
@@ -433,6 +436,7 @@ __global__ void __launch_bounds__(kThreads)
                         int64_t cols, const uint8_t *__restrict__ zflag,
                         const uint16_t *__restrict__ scales, const uint16_t *__restrict__ offsets,
                         uint8_t *__restrict__ codes) {
+  pdl_entry();
   const int64_t nbytes = (n + 1) / 2;
   for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
        b += static_cast<int64_t>(gridDim.x) * kThreads) {
@@ -465,6 +469,7 @@ __global__ void __launch_bounds__(kThreads)
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
     outlier_gather(const void *__restrict__ x, OutlierSide side) {
+  pdl_entry();
   gather_side<DT>(x, side, blockIdx.x, gridDim.x);
 }
 
@@ -473,6 +478,7 @@ __global__ void __launch_bounds__(kThreads)
     group_dequant_generic(const uint8_t *__restrict__ codes, const uint16_t *__restrict__ scales,
                           const uint16_t *__restrict__ offsets, int64_t n, int64_t g, bool pc,
                           int64_t rows, int64_t cols, void *__restrict__ y) {
+  pdl_entry();
   for (int64_t e = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; e < n;
        e += static_cast<int64_t>(gridDim.x) * kThreads) {
     const int64_t r = e / cols, c = e - r * cols;
@@ -491,6 +497,7 @@ __global__ void __launch_bounds__(kThreads)
     outlier_scatter(const uint32_t *__restrict__ idx, const uint16_t *__restrict__ val,
                     const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                     void *__restrict__ y) {
+  pdl_entry();
   // blockIdx.y walks the ranks, x the rows: no division, coalesced side-buffer reads
   const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
   for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
@@ -610,13 +617,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
     uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
-        group_quant_fast<DT, true, LL, false, 32, kU32><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, true, LL, false, 32, kU32>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 32, kU32><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, true, 32, kU32>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
-        group_quant_fast<DT, false, LL, false, 32, kU32><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, false, 32, kU32>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
@@ -630,13 +637,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
     uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
-        group_quant_fast<DT, true, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, true, LL, false, 16, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 16, kUnroll><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, true, 16, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
-        group_quant_fast<DT, false, LL, false, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, false, 16, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
@@ -650,13 +657,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
     uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
     ADC_DT_SWITCH(dt, DT, ADC_L_SWITCH(L, LL, {
       if (asym) {
-        group_quant_fast<DT, true, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, true, LL, false, 8, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        group_quant_fast<DT, false, LL, true, 8, kUnroll><<<grid + side.n_gather, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, true, 8, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
-        group_quant_fast<DT, false, LL, false, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_quant_fast<DT, false, LL, false, 8, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, nullptr, err), note_launches(1);
       }
     }));
@@ -668,15 +675,15 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
   const int gq = grid_for(c, (n + 1) / 2, kThreads);
   ADC_DT_SWITCH(dt, DT, {
     if (asym) {
-      group_stats_generic<DT, true><<<gs, kThreads, 0, c.stream>>>(
+      launch_k(group_stats_generic<DT, true>, gs, kThreads, 0, c.stream, 
           x, n, g, n_groups, pc, rows, cols, zero_flag, scales, offsets, err), note_launches(1);
-      group_quant_generic<DT, true><<<gq, kThreads, 0, c.stream>>>(x, n, g, pc, rows, cols,
+      launch_k(group_quant_generic<DT, true>, gq, kThreads, 0, c.stream, x, n, g, pc, rows, cols,
                                                                     zero_flag, scales, offsets,
                                                                     codes), note_launches(1);
     } else {
-      group_stats_generic<DT, false><<<gs, kThreads, 0, c.stream>>>(
+      launch_k(group_stats_generic<DT, false>, gs, kThreads, 0, c.stream, 
           x, n, g, n_groups, pc, rows, cols, zero_flag, scales, nullptr, err), note_launches(1);
-      group_quant_generic<DT, false><<<gq, kThreads, 0, c.stream>>>(x, n, g, pc, rows, cols,
+      launch_k(group_quant_generic<DT, false>, gq, kThreads, 0, c.stream, x, n, g, pc, rows, cols,
                                                                      zero_flag, scales, nullptr,
                                                                      codes), note_launches(1);
     }
@@ -690,7 +697,7 @@ int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *i
                           uint16_t *outl_val) {
   const OutlierSide side = outlier_side(c, idx, k_dev, k_cap, rows, cols, outl_val);
   if (side.n_gather == 0) return 0;
-  ADC_DT_SWITCH(dt, DT, outlier_gather<DT><<<side.n_gather, kThreads, 0, c.stream>>>(x, side),
+  ADC_DT_SWITCH(dt, DT, launch_k(outlier_gather<DT>, side.n_gather, kThreads, 0, c.stream, x, side),
                 note_launches(1));
   return 0;
 }
@@ -716,10 +723,10 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
     const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
     ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
       if (asym)
-        group_dequant_fast<OT, true, LL, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_dequant_fast<OT, true, LL, 8, kUnroll>, grid, kThreads, 0, c.stream, 
             codes32, scales, offsets, n_units, y), note_launches(1);
       else
-        group_dequant_fast<OT, false, LL, 8, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_dequant_fast<OT, false, LL, 8, kUnroll>, grid, kThreads, 0, c.stream, 
             codes32, scales, nullptr, n_units, y), note_launches(1);
     }));
     return 0;
@@ -731,10 +738,10 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
     const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
     ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
       if (asym)
-        group_dequant_fast<OT, true, LL, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_dequant_fast<OT, true, LL, 16, kUnroll>, grid, kThreads, 0, c.stream, 
             codes32, scales, offsets, n_units, y), note_launches(1);
       else
-        group_dequant_fast<OT, false, LL, 16, kUnroll><<<grid, kThreads, 0, c.stream>>>(
+        launch_k(group_dequant_fast<OT, false, LL, 16, kUnroll>, grid, kThreads, 0, c.stream, 
             codes32, scales, nullptr, n_units, y), note_launches(1);
     }));
     return 0;
@@ -742,10 +749,10 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
   const int grid = grid_for(c, n, kThreads);
   ADC_OT_SWITCH(ot, OT, {
     if (asym)
-      group_dequant_generic<OT, true><<<grid, kThreads, 0, c.stream>>>(codes, scales, offsets, n,
+      launch_k(group_dequant_generic<OT, true>, grid, kThreads, 0, c.stream, codes, scales, offsets, n,
                                                                        g, pc, rows, cols, y), note_launches(1);
     else
-      group_dequant_generic<OT, false><<<grid, kThreads, 0, c.stream>>>(codes, scales, nullptr,
+      launch_k(group_dequant_generic<OT, false>, grid, kThreads, 0, c.stream, codes, scales, nullptr,
                                                                         n, g, pc, rows, cols, y), note_launches(1);
   });
   return 0;
@@ -759,7 +766,7 @@ int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *va
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((rows + 4 * kThreads - 1) / (4 * kThreads), 64));
   const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(k_cap, std::max<int64_t>(1, 8 * c.num_sms / gx)));
   const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(std::min<int64_t>(gy, 65535)));
-  ADC_OT_SWITCH(ot, OT, outlier_scatter<OT><<<grid, kThreads, 0, c.stream>>>(
+  ADC_OT_SWITCH(ot, OT, launch_k(outlier_scatter<OT>, grid, kThreads, 0, c.stream, 
                             idx, val, k_dev, k_cap, rows, cols, y), note_launches(1));
   return 0;
 }

@@ -26,6 +26,27 @@ inline FastDiv make_fastdiv(uint32_t d) {
 // Count of kernels this library has launched (adc_kernel_launches()).
 void note_launches(int n);
 
+// Kernel launches go through launch_k: cudaLaunchKernelEx with programmatic
+// stream serialisation (PDL, see pdl_entry() in common.cuh) when enabled by
+// ADC_PDL=1 / adc_set_option("pdl", 1).
+bool pdl_enabled();
+void set_pdl(int v);
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct Ctx {
   cudaStream_t stream;
   int num_sms;

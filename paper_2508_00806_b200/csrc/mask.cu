@@ -94,6 +94,7 @@ template <int DT, bool FAST>
 __global__ void __launch_bounds__(kThreads)
     mask_pack(const void *__restrict__ m, int64_t n, uint8_t *__restrict__ bits,
               uint32_t *__restrict__ err) {
+  pdl_entry();
   const int64_t nbytes = (n + 7) / 8;
   bool bad = false;
   for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
@@ -113,6 +114,7 @@ __global__ void __launch_bounds__(kThreads)
 template <bool FAST>
 __global__ void __launch_bounds__(kThreads)
     mask_unpack(const uint8_t *__restrict__ bits, int64_t n, uint8_t *__restrict__ out) {
+  pdl_entry();
   const int64_t nbytes = (n + 7) / 8;
   for (int64_t b = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; b < nbytes;
        b += static_cast<int64_t>(gridDim.x) * kThreads) {
@@ -139,9 +141,9 @@ int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bi
 #define ADC_MASK_CASE(DT)                                                                    \
   case DT:                                                                                   \
     if (fast)                                                                                \
-      mask_pack<DT, true><<<grid, kThreads, 0, c.stream>>>(m, n, bits, err), note_launches(1);                 \
+      launch_k(mask_pack<DT, true>, grid, kThreads, 0, c.stream, m, n, bits, err), note_launches(1);                 \
     else                                                                                     \
-      mask_pack<DT, false><<<grid, kThreads, 0, c.stream>>>(m, n, bits, err), note_launches(1);                \
+      launch_k(mask_pack<DT, false>, grid, kThreads, 0, c.stream, m, n, bits, err), note_launches(1);                \
     break;
   switch (dt) {
     ADC_MASK_CASE(ADC_U8)
@@ -158,9 +160,9 @@ int launch_mask_unpack(const Ctx &c, const uint8_t *bits, int64_t n, uint8_t *ou
   const bool fast = n % 8 == 0 && reinterpret_cast<uintptr_t>(out) % 8 == 0;
   const int grid = grid_of(c, (n + 7) / 8);
   if (fast)
-    mask_unpack<true><<<grid, kThreads, 0, c.stream>>>(bits, n, out), note_launches(1);
+    launch_k(mask_unpack<true>, grid, kThreads, 0, c.stream, bits, n, out), note_launches(1);
   else
-    mask_unpack<false><<<grid, kThreads, 0, c.stream>>>(bits, n, out), note_launches(1);
+    launch_k(mask_unpack<false>, grid, kThreads, 0, c.stream, bits, n, out), note_launches(1);
   return 0;
 }
 

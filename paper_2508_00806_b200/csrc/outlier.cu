@@ -82,6 +82,7 @@ __device__ void numpy_order_sums(const void *x, int64_t rows, int64_t cols, doub
 
 template <int DT, bool SUM>
 __global__ void __launch_bounds__(kThreads, 3) colreduce(const void *__restrict__ x, ColArgs a) {
+  pdl_entry();
   // stage A reduction buffer; the last CTA reuses it for S and the stats scratch
   __shared__ __align__(16) unsigned char s_buf[kTailSmem];
   static_assert(kTailSmem >= kRowLanes * 32 * 8 * sizeof(double), "stage A buffer");
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(kThreads, 3) colreduce(const void *__restrict_
 // ---------------------------------------------------------------------------
 template <int DT, bool SUM>
 __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restrict__ x, ColArgs a) {
+  pdl_entry();
   __shared__ __align__(16) unsigned char s_raw[kStatsScratch];
   __shared__ int s_last;
   for (int64_t c = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; c < a.cols;
@@ -326,12 +328,12 @@ int launch_colstats_sum(const Ctx &c, const void *x, int dt, int64_t rows, int64
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
       const dim3 g = col_grid(c, colreduce<DT, true>, rows, cols);
-      colreduce<DT, true><<<g, kThreads, 0, c.stream>>>(x, a);
+      launch_k(colreduce<DT, true>, g, kThreads, 0, c.stream, x, a);
       note_launches(1);
     });
   } else {
     const int g = static_cast<int>((cols + kThreads - 1) / kThreads);
-    ADC_DT_SWITCH(dt, DT, (colstats_generic<DT, true><<<g, kThreads, 0, c.stream>>>(x, a), note_launches(1)));
+    ADC_DT_SWITCH(dt, DT, (launch_k(colstats_generic<DT, true>, g, kThreads, 0, c.stream, x, a), note_launches(1)));
   }
   return 0;
 }
@@ -343,12 +345,12 @@ int launch_colstats_max(const Ctx &c, const void *x, int dt, int64_t rows, int64
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
       const dim3 g = col_grid(c, colreduce<DT, false>, rows, cols);
-      colreduce<DT, false><<<g, kThreads, 0, c.stream>>>(x, a);
+      launch_k(colreduce<DT, false>, g, kThreads, 0, c.stream, x, a);
       note_launches(1);
     });
   } else {
     const int g = static_cast<int>((cols + kThreads - 1) / kThreads);
-    ADC_DT_SWITCH(dt, DT, (colstats_generic<DT, false><<<g, kThreads, 0, c.stream>>>(x, a), note_launches(1)));
+    ADC_DT_SWITCH(dt, DT, (launch_k(colstats_generic<DT, false>, g, kThreads, 0, c.stream, x, a), note_launches(1)));
   }
   return 0;
 }

@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(kStreamThreads, 2)
                     FastDiv dc, const uint8_t *__restrict__ zflag,
                     uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                     uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
+  pdl_entry();
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
   constexpr int EB = Loader<DT>::kBytes;
@@ -227,7 +228,7 @@ static int launch_one(const Ctx &c, const void *x, int64_t n, int64_t n_units, i
   const int64_t n_tiles = (n + kTileElems - 1) / kTileElems;
   int64_t grid = static_cast<int64_t>(c.num_sms) * 2;
   if (grid > n_tiles) grid = n_tiles;
-  group_quant_tma<DT, ASYM, L, ZERO><<<static_cast<int>(grid), kStreamThreads, kStreamSmem, c.stream>>>(
+  launch_k(group_quant_tma<DT, ASYM, L, ZERO>, static_cast<int>(grid), kStreamThreads, kStreamSmem, c.stream, 
       x, n, n_units, n_units_pad, dc, zflag, codes, scales, offsets, err);
   note_launches(1);
   return 0;
