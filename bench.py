@@ -216,6 +216,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     import torch.distributed as dist
     import paper_2508_00806_b200 as adc
     from paper_2508_00806_b200 import _lib
+    from paper_2508_00806_b200.dist_utils import whole_job_rate
     from paper_2508_00806_b200.slots import CodecSlot
     from paper_2508_00806_b200.workload import gpt_block_ops, synth_activation
 
@@ -301,11 +302,8 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     if world > 1:
         dist.barrier()
     ms = t_start.elapsed_time(t_end)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms_max = float(ms_t.item())
-    value = world * bytes_step * args.steps / (ms_max / 1e3) / 1e9
+    # whole-job GB/s: the bytes of all ranks over the MAX-over-ranks device time
+    value, ms_max = whole_job_rate(bytes_step * args.steps / 1e9, ms, dev)
 
     # ---- per-call breakdown: the same calls replayed one graph at a time with
     # CUDA events between them on the launching stream (K' steps)
@@ -372,10 +370,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         e2e_step()
     e1.record(stream)
     torch.cuda.synchronize()
-    e_ms = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e_ms, op=dist.ReduceOp.MAX)
-    e2e_value = world * bytes_step * e2e_steps / (float(e_ms.item()) / 1e3) / 1e9
+    e2e_value, _ = whole_job_rate(bytes_step * e2e_steps / 1e9, e0.elapsed_time(e1), dev)
 
     training = None
     if not args.no_train:

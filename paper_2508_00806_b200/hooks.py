@@ -136,7 +136,9 @@ class ActivationPolicy:
         self._bases.clear()
         self.records = {}
         self.measured = {}
-        if self.status is None:
+        if self.status is None and torch.cuda.is_available():
+            # shared error word of this policy's codec calls (CPU runs -- the
+            # gloo tests -- never compress: pack() keeps non-CUDA tensors)
             self.status = torch.zeros(2, dtype=torch.int32, device="cuda")
         with torch.autograd.graph.saved_tensors_hooks(self.pack, self.unpack):
             yield

@@ -24,6 +24,7 @@ import torch
 import torch.distributed as dist
 
 from . import policy as P
+from .dist_utils import broadcast_plan
 from .gpt import BLOCK_OPS, GPT, GPTConfig, synthetic_batch
 from .hooks import COMPRESS, RECOMPUTE, RETAIN, ActivationPolicy
 from .profiler import profile_model
@@ -58,10 +59,11 @@ class Trainer:
         self.net = model
         if ddp:
             from torch.nn.parallel import DistributedDataParallel as DDP
-            self.net = DDP(model, device_ids=[self.device.index], gradient_as_bucket_view=True,
-                           bucket_cap_mb=64)
+            on_gpu = self.device.type == "cuda"
+            self.net = DDP(model, device_ids=[self.device.index] if on_gpu else None,
+                           gradient_as_bucket_view=True, bucket_cap_mb=64)
         self.opt = torch.optim.AdamW(model.parameters(), lr=lr, betas=(0.9, 0.95), weight_decay=0.1,
-                                     fused=True)
+                                     fused=self.device.type == "cuda")
         self.pol = ActivationPolicy(BLOCK_OPS)
         self.step_id = 0
 
@@ -120,6 +122,7 @@ def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 6)
             plan = P.solve(p).by_op([o.op_id for o in BLOCK_OPS])
         except P.InfeasibleError:
             plan = plan_for("full-recompute")
+        plan = broadcast_plan(plan)  # rank-local profiles differ slightly: rank 0 decides
         tr.pol.plan = plan
         tr.model.load_state_dict(snap_model)
         tr.opt.load_state_dict(_clone_state(snap_opt))
@@ -183,7 +186,7 @@ def run(args) -> dict:
     snap_model = {k: v.detach().clone() for k, v in tr.model.state_dict().items()}
     snap_opt = _clone_state(tr.opt.state_dict())
     for strategy in args.policy.split(","):
-        plan = plan_for(strategy, prof)
+        plan = broadcast_plan(plan_for(strategy, prof))
         calib = []
         if strategy == "adacc" and cap < total_hbm:
             plan, calib = _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world)
