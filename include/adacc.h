@@ -89,6 +89,9 @@ ADC_API unsigned long long adc_kernel_launches(void);
 /*
  * Kernel-path selection (tuning / A-B testing; results are identical):
  *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
+ *   "outlier_spec"  1 = speculative first pass of the two-launch outlier path
+ *                   (column sums + quantisation with the previous call's
+ *                   channel set in one read; 0 default).  ADC_OUTLIER_SPEC=1.
  *   "pdl"           1 = launch with programmatic dependent launch (0 default).
  *   "epl"           32 (default) or 16 elements per lane in the group
  *                   quantisers (also ADC_EPL=16).

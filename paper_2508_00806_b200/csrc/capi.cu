@@ -111,6 +111,10 @@ int adc_set_option(const char *key, int value) {
     set_compress_path(value);
     return ADC_OK;
   }
+  if (k == "outlier_spec") {  // speculative single-read first pass (1) / plain two launches (0, default)
+    set_outlier_spec(value);
+    return ADC_OK;
+  }
   if (k == "pdl") {  // programmatic dependent launch on (1) / off (0, default)
     set_pdl(value);
     return ADC_OK;
@@ -200,6 +204,14 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
     if (launch_outlier_fused(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
                              codes, scales, outlier_idx, outlier_val, k_out, err_word))
       return check_launch("outlier_fused");
+    if (k_cap > 0 && launch_outlier_spec(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
+                                         codes, scales, outlier_idx, k_out, err_word, ws.counters + 3)) {
+      rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag, outlier_idx,
+                                  k_out, outlier_val, k_cap, codes, scales, nullptr, err_word,
+                                  ws.counters + 3);
+      if (rc) return fail(ADC_EINVAL, "outlier dispatch");
+      return check_launch("outlier_speculative");
+    }
     rc |= launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap,
                               outlier_idx, k_out, err_word, true);
     rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag,

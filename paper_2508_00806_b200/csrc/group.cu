@@ -47,6 +47,7 @@ struct OutlierSide {
   int64_t k_cap, rows, cols;
   uint16_t *val;
   int n_gather;  // leading CTAs that gather (0: none)
+  const uint32_t *requant;  // non-null: quantise only if *requant != 0 (speculation missed)
 };
 constexpr int kGatherRanks = 8;
 
@@ -154,6 +155,9 @@ __global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
     }
     cta -= side.n_gather;
     n_ctas -= side.n_gather;
+    // the speculative column-statistics kernel already wrote codes / scales
+    // with the predicted channel set; re-quantise only if it missed
+    if (side.requant && __ldcg(side.requant) == 0u) return;
   }
   const int64_t step = n_ctas * kThreads * U;
   for (int64_t base = cta * kThreads * U; base < n_units_pad; base += step) {
@@ -585,7 +589,7 @@ constexpr int kU32 = 1;  // units in flight per lane at 32 elements per lane
 // one CTA per SM (the gather is latency-bound and short).
 static OutlierSide outlier_side(const Ctx &c, const uint32_t *idx, const int32_t *k_dev,
                                 int64_t k_cap, int64_t rows, int64_t cols, uint16_t *val) {
-  OutlierSide o{idx, k_dev, k_cap, rows, cols, val, 0};
+  OutlierSide o{idx, k_dev, k_cap, rows, cols, val, 0, nullptr};
   if (k_cap <= 0 || !val || !idx || !k_dev) return o;
   const int64_t items = ((rows + kThreads - 1) / kThreads) * ((k_cap + kGatherRanks - 1) / kGatherRanks);
   o.n_gather = static_cast<int>(items < c.num_sms ? items : c.num_sms);
@@ -595,13 +599,14 @@ static OutlierSide outlier_side(const Ctx &c, const uint32_t *idx, const int32_t
 int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
                           int64_t g, bool asym, const uint8_t *zero_flag, const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
                           int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
-                          uint32_t *err) {
+                          uint32_t *err, const uint32_t *requant) {
   const int64_t n = rows * cols;
   const bool pc = (g == 0);
   const bool zero = zero_flag != nullptr;
   const bool zero_ok = !zero || (cols % 8 == 0 && n < (1ll << 31));
   const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
-  const OutlierSide side = outlier_side(c, idx, k_dev, zero ? k_cap : 0, rows, cols, outl_val);
+  OutlierSide side = outlier_side(c, idx, k_dev, zero ? k_cap : 0, rows, cols, outl_val);
+  side.requant = zero ? requant : nullptr;
   int L = pc ? 0 : lanes_for_group(g, 8);
   if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok) {
     const int rc = launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, codes,

@@ -76,7 +76,7 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base);
 int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
                           int64_t g, bool asym, const uint8_t *zero_flag, const uint32_t *idx, const int32_t *k_dev, uint16_t *outl_val,
                           int64_t k_cap, uint8_t *codes, uint16_t *scales, uint16_t *offsets,
-                          uint32_t *err);
+                          uint32_t *err, const uint32_t *requant = nullptr);
 int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
                             const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
                             bool asym, void *y, int ot);
@@ -111,6 +111,18 @@ bool use_fused_outlier();
 void set_fused_outlier(int v);
 void set_fused_trace(int v);
 int read_fused_trace(unsigned long long *host, int n);
+
+// Speculative outlier-separated first pass (spec.cu): column sums AND the
+// symmetric quantisation with the previous call's channel set (ws.pflag) in
+// one read of x; the last CTA computes the statistics and writes *miss = 1
+// when the actual channel set differs (then the quantiser launch redoes the
+// codes).  Returns 0 if the shape is not eligible.
+int launch_outlier_spec(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols, int64_t g,
+                        double thr, int64_t k_cap, const Workspace &ws, uint8_t *codes,
+                        uint16_t *scales, uint32_t *idx, int32_t *k_out, uint32_t *err,
+                        uint32_t *miss);
+bool use_outlier_spec();
+void set_outlier_spec(int v);
 
 // per-channel kernels (channel.cu)
 bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,

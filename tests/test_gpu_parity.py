@@ -352,11 +352,13 @@ def test_fused_outlier_matches_two_launch_path(torch_cuda, shape, dtype_name, gr
     assert ct.outlier_count == (0 if idx is None else len(idx))
 
 
-@pytest.mark.parametrize("dtype_name,cols", [("bfloat16", 1024), ("float32", 768), ("float16", 4096)])
-def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols):
+@pytest.mark.parametrize("path", ["fused", "speculative"])
+@pytest.mark.parametrize("dtype_name,cols", [("bfloat16", 1024), ("float32", 768), ("float16", 4096),
+                                             ("bfloat16", 3072)])
+def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, path):
     """A slot's workspace carries the previous call's channel set; the fused
-    kernel quantises speculatively with it and re-quantises when the actual
-    set differs.  Alternate inputs with different / equal outlier sets
+    kernel (or the speculative first pass of the two-launch path) quantises
+    with it and re-quantises when the actual set differs.  Alternate inputs with different / equal outlier sets
     through ONE slot and check every call against the oracle."""
     torch = torch_cuda
     import paper_2508_00806_b200 as adc
@@ -368,7 +370,8 @@ def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols):
     seq = [0, 0, 1, 1, 0, 2, 2, 1, 0]
     dt = getattr(torch, dtype_name)
     from paper_2508_00806_b200 import _lib
-    _lib.set_option("outlier_path", 1)
+    _lib.set_option("outlier_path", 1 if path == "fused" else 2)
+    _lib.set_option("outlier_spec", 1 if path == "speculative" else 0)
     slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), dt, torch.float32, k_cap=64)
     y = torch.empty(rows, cols, dtype=torch.float32, device="cuda")
     for step, si in enumerate(seq):
@@ -392,3 +395,4 @@ def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols):
         np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), wdeq.view(np.uint32))
         assert int(slot.status[0]) == 0
     _lib.set_option("outlier_path", 2)
+    _lib.set_option("outlier_spec", 0)
