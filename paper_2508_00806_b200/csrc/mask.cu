@@ -4,6 +4,8 @@
 // (NonBinaryMaskError otherwise), bit (i mod 8) of byte i/8 = m[i]
 // (np.packbits bitorder="little"), zero padding; unpack_bitmask (:372-378).
 // One thread packs 64 elements into one 64-bit word.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "launch.h"
 
@@ -127,6 +129,68 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Wide variants for byte masks (bool tensors, the training case): a thread
+// packs 32 elements (two 128-bit loads -> one 32-bit store) / expands 32 bits
+// into 32 bytes (one 32-bit load -> two 128-bit stores), two units in flight.
+__global__ void __launch_bounds__(kThreads)
+    mask_pack_u8x32(const uint4 *__restrict__ m, int64_t units, uint32_t *__restrict__ bits,
+                    uint32_t *__restrict__ err) {
+  pdl_entry();
+  bool bad = false;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t u = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; u < units; u += 2 * stride) {
+    uint4 v[2][2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t uq = u + q * stride;
+      v[q][0] = uq < units ? __ldcs(m + 2 * uq) : make_uint4(0, 0, 0, 0);
+      v[q][1] = uq < units ? __ldcs(m + 2 * uq + 1) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t uq = u + q * stride;
+      if (uq >= units) continue;
+      const uint32_t w[8] = {v[q][0].x, v[q][0].y, v[q][0].z, v[q][0].w,
+                             v[q][1].x, v[q][1].y, v[q][1].z, v[q][1].w};
+      uint32_t r = 0, any = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        any |= w[j];
+        r |= gather4(w[j]) << (4 * j);
+      }
+      bad |= (any & 0xfefefefeu) != 0;
+      __stcs(bits + uq, r);
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) raise_err(err, ADC_ERR_NONBINARY);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    mask_unpack_u8x32(const uint32_t *__restrict__ bits, int64_t units, uint4 *__restrict__ out) {
+  pdl_entry();
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * kThreads;
+  for (int64_t u = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; u < units; u += 2 * stride) {
+    uint32_t v[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) v[q] = u + q * stride < units ? __ldcs(bits + u + q * stride) : 0u;
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int64_t uq = u + q * stride;
+      if (uq >= units) continue;
+      const uint32_t b = v[q];
+      st_stream16(out + 2 * uq, make_uint4(spread4(b & 0xfu), spread4((b >> 4) & 0xfu),
+                                           spread4((b >> 8) & 0xfu), spread4((b >> 12) & 0xfu)));
+      st_stream16(out + 2 * uq + 1, make_uint4(spread4((b >> 16) & 0xfu), spread4((b >> 20) & 0xfu),
+                                               spread4((b >> 24) & 0xfu), spread4(b >> 28)));
+    }
+  }
+}
+
+static bool use_wide_unpack() {
+  const char *e = getenv("ADC_MASK_WIDE_UNPACK");
+  return e && e[0] == '1';
+}
+
 static inline int grid_of(const Ctx &c, int64_t items) {
   int64_t need = (items + kThreads - 1) / kThreads;
   int64_t cap = static_cast<int64_t>(c.num_sms) * 16;
@@ -137,6 +201,15 @@ int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bi
                      uint32_t *err) {
   const int elt = dt == ADC_F32 ? 4 : (dt == ADC_U8 ? 1 : 2);
   const bool fast = n % 8 == 0 && reinterpret_cast<uintptr_t>(m) % (8 * elt < 16 ? 8 * elt : 16) == 0;
+  if (dt == ADC_U8 && n % 32 == 0 && reinterpret_cast<uintptr_t>(m) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(bits) % 4 == 0) {
+    const int64_t units = n / 32;
+    const int g = grid_of(c, (units + 1) / 2);
+    launch_k(mask_pack_u8x32, g, kThreads, 0, c.stream, reinterpret_cast<const uint4 *>(m), units,
+             reinterpret_cast<uint32_t *>(bits), err);
+    note_launches(1);
+    return 0;
+  }
   const int grid = grid_of(c, (n + 7) / 8);
 #define ADC_MASK_CASE(DT)                                                                    \
   case DT:                                                                                   \
@@ -157,6 +230,16 @@ int launch_mask_pack(const Ctx &c, const void *m, int dt, int64_t n, uint8_t *bi
 }
 
 int launch_mask_unpack(const Ctx &c, const uint8_t *bits, int64_t n, uint8_t *out) {
+  // mask_unpack_u8x32 measured slower (39 vs 33 us at 134 MB): the byte-per-thread kernel stays
+  if (use_wide_unpack() && n % 32 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0 &&
+      reinterpret_cast<uintptr_t>(bits) % 4 == 0) {
+    const int64_t units = n / 32;
+    const int g = grid_of(c, (units + 1) / 2);
+    launch_k(mask_unpack_u8x32, g, kThreads, 0, c.stream, reinterpret_cast<const uint32_t *>(bits), units,
+             reinterpret_cast<uint4 *>(out));
+    note_launches(1);
+    return 0;
+  }
   const bool fast = n % 8 == 0 && reinterpret_cast<uintptr_t>(out) % 8 == 0;
   const int grid = grid_of(c, (n + 7) / 8);
   if (fast)
