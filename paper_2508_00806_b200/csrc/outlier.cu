@@ -85,7 +85,7 @@ __device__ void numpy_order_sums(const void *x, int64_t rows, int64_t cols, doub
 }
 
 template <int DT, bool SUM>
-__global__ void __launch_bounds__(kThreads, 3) colreduce(const void *__restrict__ x, ColArgs a) {
+__global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict__ x, ColArgs a) {
   pdl_entry();
   // stage A reduction buffer; the last CTA reuses it for S and the stats scratch
   __shared__ __align__(16) unsigned char s_buf[kTailSmem];
