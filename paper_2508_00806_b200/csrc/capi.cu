@@ -266,7 +266,8 @@ int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
   if (rc) return fail(ADC_EINVAL, "decompress dispatch");
   if (scheme == ADC_OUTLIER_SEPARATED && k_cap > 0) {
     if (!outlier_idx || !outlier_val || !k_dev) return fail(ADC_EINVAL, "outlier buffers required");
-    launch_outlier_scatter(c, outlier_idx, outlier_val, k_dev, k_cap, rows, cols, y, out_dtype);
+    launch_outlier_scatter(c, outlier_idx, outlier_val, k_dev, k_cap, rows, cols, y, out_dtype,
+                           pc ? nullptr : codes, scales, group_size);
   }
   return check_launch("decompress");
 }

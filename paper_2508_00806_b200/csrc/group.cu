@@ -513,6 +513,53 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Outlier overwrite after the plain dequantisation (codec.py:284-285), one
+// thread per (rank, row) rewriting the whole 32-byte sector that holds the
+// flagged element: 16 dequantised values (their 128-group's scale; sectors
+// never straddle a group) with the stored float16 values of every flagged
+// channel in that sector.  Full-sector stores avoid the read-modify-write a
+// 2-byte scatter costs once the output has left L2 (k x rows partial sectors).
+// The first rank of a sector owns it.  Ranks on grid.y, rows on grid.x.
+template <int OT, int L>
+__global__ void __launch_bounds__(kThreads)
+    outlier_patch16(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
+                    const uint32_t *__restrict__ idx, const uint16_t *__restrict__ val,
+                    const int32_t *__restrict__ k_dev, int64_t k_cap, int64_t rows, int64_t cols,
+                    void *__restrict__ y) {
+  pdl_entry();
+  constexpr int SE = 32 / Storer<OT>::kBytes;  // elements per 32-byte sector (16 bf16/f16, 8 f32)
+  const int64_t k = min(static_cast<int64_t>(*k_dev), k_cap);
+  for (int64_t j = blockIdx.y; j < k; j += gridDim.y) {
+    const uint32_t c = __ldg(idx + j);
+    const uint32_t sec = c / SE;
+    if (j > 0 && __ldg(idx + j - 1) / SE == sec) continue;  // an earlier rank owns this sector
+    int nj = 1;                                             // ranks in this sector: j .. j + nj - 1
+    while (j + nj < k && nj < SE && __ldg(idx + j + nj) / SE == sec) ++nj;
+    for (int64_t r = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; r < rows;
+         r += static_cast<int64_t>(gridDim.x) * kThreads) {
+      const int64_t e0 = r * cols + static_cast<int64_t>(sec) * SE;  // first element of the sector
+      const int64_t u0 = e0 / 8;                                     // its first 8-element code word
+      float v[16];
+      const float sc = h2f(__ldg(scales + e0 / (8 * L)));
+#pragma unroll
+      for (int h = 0; h < SE / 8; ++h) {
+        const uint32_t w = __ldg(codes + u0 + h);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[8 * h + q] = deq<false>(nib_code(w, q), sc, 0.f);
+      }
+      for (int t = 0; t < nj; ++t) {
+        const uint32_t cc = __ldg(idx + j + t) - sec * SE;
+        const float hv = h2f(__ldg(val + (j + t) * rows + r));
+#pragma unroll
+        for (int q = 0; q < SE; ++q)
+          if (q == static_cast<int>(cc)) v[q] = hv;
+      }
+#pragma unroll
+      for (int h = 0; h < SE / 8; ++h) Storer<OT>::store8(y, e0 + 8 * h, v + 8 * h);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
@@ -765,8 +812,30 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
 
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
-                           void *y, int ot) {
+                           void *y, int ot, const uint8_t *codes, const uint16_t *scales, int64_t g) {
   if (k_cap <= 0) return 0;
+  // whole-sector patches when the output is too large to still sit in L2
+  // (then a 2-byte scatter pays a DRAM read-modify-write per element;
+  // measured 127.7 -> 105.9 us for [131072,1024] bf16, k = 11) and the codes
+  // are row-major groups that never straddle a 32-byte output sector; small
+  // outputs keep the scatter (one dependent load instead of two: 8.3 vs
+  // 12.9 us at [8192,1024])
+  const int se = ot == ADC_F32 ? 8 : 16;
+  const int L = codes && scales ? lanes_for_group(g, 8) : 0;
+  const int64_t out_bytes = rows * cols * (ot == ADC_F32 ? 4 : 2);
+  if (L > 0 && out_bytes > (128ll << 20) && g % se == 0 && cols % se == 0 && aligned(y, 32) &&
+      aligned(codes, 4)) {
+    const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((rows + 4 * kThreads - 1) / (4 * kThreads), 64));
+    const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(k_cap, std::max<int64_t>(1, 8 * c.num_sms / gx)));
+    const dim3 grid(static_cast<unsigned>(gx), static_cast<unsigned>(std::min<int64_t>(gy, 65535)));
+    const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
+    ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
+      launch_k(outlier_patch16<OT, LL>, grid, kThreads, 0, c.stream, codes32, scales, idx, val, k_dev,
+               k_cap, rows, cols, y);
+      note_launches(1);
+    }));
+    return 0;
+  }
   // ~4 rows per thread, ranks across grid.y (at most ~4 waves of CTAs)
   const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((rows + 4 * kThreads - 1) / (4 * kThreads), 64));
   const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(k_cap, std::max<int64_t>(1, 8 * c.num_sms / gx)));

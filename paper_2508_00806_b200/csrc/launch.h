@@ -82,7 +82,8 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
                             bool asym, void *y, int ot);
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
-                           void *y, int ot);
+                           void *y, int ot, const uint8_t *codes = nullptr,
+                           const uint16_t *scales = nullptr, int64_t g = 0);
 
 // TMA-fed streaming variant of the fast group compress (stream.cu); L = lanes
 // per group at 8 elements per lane.

@@ -396,3 +396,31 @@ def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, 
         assert int(slot.status[0]) == 0
     _lib.set_option("outlier_path", 2)
     _lib.set_option("outlier_spec", 0)
+
+
+@pytest.mark.parametrize("rows", [16384, 16384 + 256])
+def test_outlier_decompress_sector_patch_large_outputs(torch_cuda, rows):
+    """Outputs past L2 take the whole-sector patch instead of the 2-byte
+    scatter: f32 (8-element sectors) and bf16 (16-element sectors) outputs
+    agree with each other and with a torch reconstruction from the payload."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    cols = 4096
+    g = torch.Generator(device="cuda").manual_seed(rows)
+    x = torch.randn(rows, cols, device="cuda", generator=g)
+    hot = torch.randperm(cols, generator=g, device="cuda")[:37]
+    hot[1] = hot[0] ^ 1  # two flagged channels in one sector
+    x[:, hot] *= 40
+    x = x.to(torch.bfloat16)
+    ct = adc.compress(x, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED))
+    y32 = adc.decompress(ct)                       # 256+ MB: patch, 8-element sectors
+    y16 = adc.decompress(ct, torch.bfloat16)       # 128+ MB: patch, 16-element sectors
+    assert torch.equal(y16.view(torch.int16), y32.to(torch.bfloat16).view(torch.int16))
+    # reference reconstruction: dequantise every code, then overwrite the flagged channels
+    nib = torch.stack([ct.packed_codes & 0xF, ct.packed_codes >> 4], dim=1).reshape(-1).to(torch.int32)
+    code = torch.where(nib >= 8, nib - 16, nib).to(torch.float32).reshape(rows, cols)
+    ref = (code.reshape(-1, 128) * ct.scales.to(torch.float32)[:, None]).reshape(rows, cols)
+    idx = ct.outlier_indices.to(torch.int64)
+    ref[:, idx] = ct.outlier_values.to(torch.float32).T
+    assert idx.numel() >= 30
+    assert torch.equal(y32.view(torch.int32), ref.view(torch.int32))
