@@ -709,7 +709,20 @@ __device__ __forceinline__ int outlier_stats_block(const double *S, int64_t rows
   if (cols <= kHeapMaxCols) {
     double *val = reinterpret_cast<double *>(scratch);
     const int D = heap_depth(n);
-    mean = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
+    // the mean's sum: when the any-order total stays below 2^29 every partial
+    // sum of numpy's tree is exact (non-negative multiples of 2^-24), so the
+    // tree equals a plain block reduction (see warp_mean_var)
+    double part = 0.0;
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) part = __dadd_rn(part, t.load(c));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+    if ((threadIdx.x & 31) == 0) val[threadIdx.x >> 5] = part;
+    __syncthreads();
+    double total = 0.0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) total = __dadd_rn(total, val[w]);
+    __syncthreads();
+    if (!(total < 536870912.0)) total = heap_sum(t, n, D, val);
+    mean = __ddiv_rn(__dadd_rn(0.0, total), static_cast<double>(cols));
     t.mean = mean;
     t.squared = true;
     var = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
