@@ -155,6 +155,22 @@ ADC_API int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *sca
                    int64_t rows, int64_t cols, int64_t group_size, void *y, int out_dtype,
                    void *stream);
 
+/*
+ * EXTENSION, no reference counterpart (north_star names int8 codes with fp32
+ * scales; the reference has only int4): symmetric group int8.
+ * Parity unpinned -- semantics defined by this library and restated in
+ * oracle/int8_oracle.py: h = f16(x); per group of group_size row-major
+ * elements s = f32(max|h| / 127); code = clip(rint_even(f32(h / s)), -127,
+ * 127) (s = 0 divides by 1); decompress = f32(code * s) (then RNE to the
+ * output dtype).  codes: rows*cols int8; scales: ceil(rows*cols/group) f32.
+ * Non-finite inputs raise ADC_ERR_NONFINITE in err_word.
+ */
+ADC_API int adc_compress_int8(const void *x, int in_dtype, int64_t rows, int64_t cols,
+                              int64_t group_size, int8_t *codes, float *scales, uint32_t *err_word,
+                              void *stream);
+ADC_API int adc_decompress_int8(const int8_t *codes, const float *scales, int64_t rows, int64_t cols,
+                                int64_t group_size, void *y, int out_dtype, void *stream);
+
 /* Column sums of |f16(x)| in float64; replaces channel_abs_sums (codec.py:289-291). */
 ADC_API int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols,
                          double *sums, uint32_t *err_word, void *workspace,

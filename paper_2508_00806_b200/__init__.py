@@ -14,6 +14,7 @@ from .codec import (
     SERIALIZED_HEADER_BYTES,
     CodecReport,
     CompressedTensor,
+    Int8Tensor,
     Scheme,
     SchemeSpec,
     channel_abs_sums,
@@ -23,6 +24,7 @@ from .codec import (
     decompress,
     decompress_into,
     dequantize,
+    dequantize_int8,
     deserialize,
     detect_outlier_channels,
     measure_codec,
@@ -30,6 +32,7 @@ from .codec import (
     pack_bitmask,
     packed_payload_bytes,
     quantize_asymmetric,
+    quantize_int8,
     quantize_symmetric,
     scheme_for,
     serialize,

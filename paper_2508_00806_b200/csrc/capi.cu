@@ -272,6 +272,29 @@ int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
   return check_launch("decompress");
 }
 
+int adc_compress_int8(const void *x, int in_dtype, int64_t rows, int64_t cols, int64_t group_size,
+                      int8_t *codes, float *scales, uint32_t *err_word, void *stream) {
+  if (rows < 1 || cols < 1) return fail(ADC_EINVAL, "activation matrix must have at least one element");
+  if (!x || !codes || !scales) return fail(ADC_EINVAL, "null buffer");
+  if (!valid_float_dtype(in_dtype)) return fail(ADC_EINVAL, "activation dtype must be f32, bf16 or f16");
+  if (group_size < 1) return fail(ADC_EINVAL, "group_size must be positive");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  if (launch_int8_compress(c, x, in_dtype, rows * cols, group_size, codes, scales, err_word))
+    return fail(ADC_EINVAL, "int8 dispatch");
+  return check_launch("int8_compress");
+}
+
+int adc_decompress_int8(const int8_t *codes, const float *scales, int64_t rows, int64_t cols,
+                        int64_t group_size, void *y, int out_dtype, void *stream) {
+  if (rows < 1 || cols < 1 || !codes || !scales || !y) return fail(ADC_EINVAL, "bad arguments");
+  if (group_size < 1) return fail(ADC_EINVAL, "group_size must be positive");
+  if (!valid_float_dtype(out_dtype)) return fail(ADC_EINVAL, "output dtype must be f32, bf16 or f16");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  if (launch_int8_decompress(c, codes, scales, rows * cols, group_size, y, out_dtype))
+    return fail(ADC_EINVAL, "int8 decompress dispatch (codes need 8-byte, output 16-byte alignment)");
+  return check_launch("int8_decompress");
+}
+
 int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols, double *sums,
                          uint32_t *err_word, void *workspace, size_t workspace_bytes,
                          void *stream) {

@@ -125,6 +125,12 @@ int launch_outlier_spec(const Ctx &c, const void *x, int dt, int64_t rows, int64
 bool use_outlier_spec();
 void set_outlier_spec(int v);
 
+// int8 extension (int8.cu; parity unpinned, oracle/int8_oracle.py)
+int launch_int8_compress(const Ctx &c, const void *x, int dt, int64_t n, int64_t g, int8_t *codes,
+                         float *scales, uint32_t *err);
+int launch_int8_decompress(const Ctx &c, const int8_t *codes, const float *scales, int64_t n, int64_t g,
+                           void *y, int ot);
+
 // per-channel kernels (channel.cu)
 bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,
                      const void *scales);
