@@ -171,6 +171,20 @@ ADC_API int adc_compress_int8(const void *x, int in_dtype, int64_t rows, int64_t
 ADC_API int adc_decompress_int8(const int8_t *codes, const float *scales, int64_t rows, int64_t cols,
                                 int64_t group_size, void *y, int out_dtype, void *stream);
 
+/*
+ * Device-side ADC1 wire format; replaces serialize (codec.py:432-459) without
+ * a host round trip: writes the 25-byte header, metadata, codes and outlier
+ * side buffer of a compressed tensor (the device buffers adc_compress wrote)
+ * into `out` (16-byte aligned device memory, out_cap bytes) and the total
+ * length into the device word *out_len.  If the payload exceeds out_cap it
+ * is truncated and ADC_ERR_K_CAP is raised in err_word.
+ */
+ADC_API int adc_serialize(int scheme, const uint16_t *scales, const uint16_t *offsets,
+                          const uint8_t *codes, const uint32_t *outlier_idx,
+                          const uint16_t *outlier_val, const int32_t *k_dev, int64_t k_cap,
+                          int64_t rows, int64_t cols, int64_t group_size, uint8_t *out,
+                          size_t out_cap, uint64_t *out_len, uint32_t *err_word, void *stream);
+
 /* Column sums of |f16(x)| in float64; replaces channel_abs_sums (codec.py:289-291). */
 ADC_API int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols,
                          double *sums, uint32_t *err_word, void *workspace,

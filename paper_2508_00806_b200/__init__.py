@@ -36,6 +36,7 @@ from .codec import (
     quantize_symmetric,
     scheme_for,
     serialize,
+    serialize_device,
     unpack_bitmask,
 )
 from .errors import (

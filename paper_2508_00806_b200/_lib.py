@@ -37,6 +37,8 @@ SIGNATURES = {
                                  _i64, _vp, C.c_int, _vp]),
     "adc_compress_int8": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "adc_decompress_int8": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, C.c_int, _vp]),
+    "adc_serialize": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
+                                _vp, _vp, _vp]),
     "adc_channel_abs_sums": (C.c_int, [_vp, C.c_int, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "adc_detect_outliers": (C.c_int, [_vp, C.c_int, _i64, _i64, C.c_double, _i64, _vp, _vp,
                                       _vp, _vp, _sz, _vp]),

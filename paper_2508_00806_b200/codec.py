@@ -553,6 +553,34 @@ def serialize(ct: CompressedTensor) -> bytes:
     return b"".join(parts)
 
 
+def serialize_device(ct: CompressedTensor) -> torch.Tensor:
+    """ADC1 bytes (codec.py:432-459) assembled on the device (adc_serialize):
+    a uint8 device tensor equal to ``serialize(ct)``."""
+    rows, cols = ct.rows, ct.cols
+    dev = (ct.mask_bits if ct.scheme is Scheme.BIT_MASK else ct.packed_codes).device
+    idx = val = kd = None
+    k_cap = 0
+    if ct.scheme is Scheme.OUTLIER_SEPARATED and ct.outlier_count:
+        if ct.outlier_indices.dtype == torch.int32 and ct.k_dev is not None:  # async record: (k_cap, rows)
+            idx, val, kd, k_cap = ct.outlier_indices, ct.outlier_values, ct.k_dev, ct.k_cap
+        else:  # parity record: trimmed to k
+            idx = ct.outlier_indices.to(torch.int32).contiguous()
+            val = ct.outlier_values.contiguous()
+            k_cap = int(idx.numel())
+            kd = torch.tensor([0, k_cap], dtype=torch.int32, device=dev)
+    cap = _HEADER.size + packed_payload_bytes(ct.scheme, rows, cols, ct.group_size, k_cap)
+    out = torch.empty((cap + 15) // 16 * 16, dtype=torch.uint8, device=dev)
+    meta = torch.zeros(2, dtype=torch.int64, device=dev)  # [length, error word]
+    codes = ct.mask_bits if ct.scheme is Scheme.BIT_MASK else ct.packed_codes
+    st = _lib.lib().adc_serialize(int(ct.scheme), _ptr(ct.scales), _ptr(ct.offsets), codes.data_ptr(),
+                                  _ptr(idx), _ptr(val), None if kd is None else kd.data_ptr() + 4, k_cap,
+                                  rows, cols, ct.group_size, out.data_ptr(), out.numel(), meta.data_ptr(),
+                                  meta.data_ptr() + 8, _stream())
+    _lib.check(st, "serialize")
+    length = int(meta[0].item())
+    return out[:length]
+
+
 def deserialize(buf: bytes) -> CompressedTensor:
     """Parse + validate an ADC1 payload onto the device (codec.py:462-546)."""
     if len(buf) < _HEADER.size:

@@ -295,6 +295,28 @@ int adc_decompress_int8(const int8_t *codes, const float *scales, int64_t rows, 
   return check_launch("int8_decompress");
 }
 
+int adc_serialize(int scheme, const uint16_t *scales, const uint16_t *offsets, const uint8_t *codes,
+                  const uint32_t *outlier_idx, const uint16_t *outlier_val, const int32_t *k_dev,
+                  int64_t k_cap, int64_t rows, int64_t cols, int64_t group_size, uint8_t *out,
+                  size_t out_cap, uint64_t *out_len, uint32_t *err_word, void *stream) {
+  int64_t n_groups = 0, code_bytes = 0;
+  if (adc_payload_bytes(scheme, rows, cols, group_size, 0, &n_groups, &code_bytes, nullptr) != ADC_OK)
+    return ADC_EINVAL;
+  if (rows > 0xffffffffll || cols > 0xffffffffll) return fail(ADC_EINVAL, "shape exceeds the u32 header fields");
+  if (!codes || !out || !out_len) return fail(ADC_EINVAL, "null buffer");
+  if (scheme != ADC_BIT_MASK && !scales) return fail(ADC_EINVAL, "null scales");
+  if (scheme == ADC_ASYMMETRIC_GROUP && !offsets) return fail(ADC_EINVAL, "null offsets");
+  const bool outl = scheme == ADC_OUTLIER_SEPARATED && k_cap > 0;
+  if (outl && (!outlier_idx || !outlier_val || !k_dev)) return fail(ADC_EINVAL, "outlier buffers required");
+  if (reinterpret_cast<uintptr_t>(out) % 16) return fail(ADC_EINVAL, "out must be 16-byte aligned");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  launch_wire_serialize(c, scheme, rows, cols, group_size, n_groups, scheme == ADC_BIT_MASK ? nullptr : scales,
+                        scheme == ADC_ASYMMETRIC_GROUP ? offsets : nullptr, codes, code_bytes,
+                        outl ? outlier_idx : nullptr, outl ? outlier_val : nullptr, outl ? k_dev : nullptr,
+                        outl ? k_cap : 0, out, static_cast<int64_t>(out_cap), out_len, err_word);
+  return check_launch("serialize");
+}
+
 int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols, double *sums,
                          uint32_t *err_word, void *workspace, size_t workspace_bytes,
                          void *stream) {

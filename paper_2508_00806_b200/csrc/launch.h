@@ -131,6 +131,13 @@ int launch_int8_compress(const Ctx &c, const void *x, int dt, int64_t n, int64_t
 int launch_int8_decompress(const Ctx &c, const int8_t *codes, const float *scales, int64_t n, int64_t g,
                            void *y, int ot);
 
+// device-side ADC1 serialisation (wire.cu)
+int launch_wire_serialize(const Ctx &c, int scheme, int64_t rows, int64_t cols, int64_t group,
+                          int64_t n_groups, const uint16_t *scales, const uint16_t *offsets,
+                          const uint8_t *codes, int64_t code_bytes, const uint32_t *idx,
+                          const uint16_t *val, const int32_t *k_dev, int64_t k_cap, uint8_t *out,
+                          int64_t out_cap, uint64_t *out_len, uint32_t *err);
+
 // per-channel kernels (channel.cu)
 bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,
                      const void *scales);

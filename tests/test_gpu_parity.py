@@ -424,3 +424,29 @@ def test_outlier_decompress_sector_patch_large_outputs(torch_cuda, rows):
     ref[:, idx] = ct.outlier_values.to(torch.float32).T
     assert idx.numel() >= 30
     assert torch.equal(y32.view(torch.int32), ref.view(torch.int32))
+
+
+@pytest.mark.parametrize("scheme,group,shape", [
+    (cases.SYM, 128, (300, 70)), (cases.ASYM, 128, (256, 768)), (cases.OUTL, 128, (512, 1024)),
+    (cases.SYM, 0, (64, 96)), (cases.MASK, 0, (33, 17)), (cases.ASYM, 7, (5, 11)), (cases.OUTL, 64, (1000, 40))])
+def test_device_serialize_matches_host_and_oracle_bytes(torch_cuda, scheme, group, shape):
+    """adc_serialize assembles the ADC1 bytes on the device: identical to the
+    host serializer and to the oracle's (reference-pinned) serializer, for
+    parity records and for async records read straight from the slot buffers."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from oracle import codec_oracle as orc
+    rng = np.random.default_rng(shape[0] * 3 + group)
+    if scheme == cases.MASK:
+        x = (rng.random(shape) < 0.7).astype(np.uint8)
+    else:
+        x = rng.normal(size=shape).astype(np.float32)
+        x[:, :: max(1, shape[1] // 9)] *= 30
+    spec = adc.SchemeSpec(adc.Scheme(scheme), group)
+    ct = adc.compress(x, spec)
+    dev_bytes = adc.serialize_device(ct).cpu().numpy().tobytes()
+    assert dev_bytes == adc.serialize(ct)
+    assert dev_bytes == orc.serialize(orc.compress(x, scheme, group, 3.0))
+    if scheme == cases.OUTL:  # async record: (k_cap, rows) buffers and the device k
+        act = adc.compress_async(torch.from_numpy(x).cuda(), spec)
+        assert adc.serialize_device(act).cpu().numpy().tobytes() == dev_bytes
