@@ -256,6 +256,12 @@ int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
   if (asym && !offsets) return fail(ADC_EINVAL, "null offsets");
   const bool pc = group_size == ADC_PER_CHANNEL;
   int rc = 0;
+  if (scheme == ADC_OUTLIER_SEPARATED && k_cap > 0 && outlier_idx && outlier_val && k_dev && !pc) {
+    rc = launch_outlier_decompress(c, codes, scales, outlier_idx, outlier_val, k_dev, k_cap, rows, cols,
+                                   group_size, y, out_dtype);
+    if (rc < 0) return fail(ADC_EINVAL, "decompress dispatch");
+    if (rc == 0) return check_launch("outlier_decompress");
+  }
   if (pc && !asym && channel_fast_ok(y, rows, cols, codes, scales) &&
       reinterpret_cast<uintptr_t>(y) % 16 == 0) {
     rc = launch_channel_decompress(c, codes, scales, rows, cols, y, out_dtype);

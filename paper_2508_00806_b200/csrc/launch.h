@@ -80,6 +80,12 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
 int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
                             const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
                             bool asym, void *y, int ot);
+// dequantise + flagged-channel overwrite in one launch (outputs within L2);
+// returns 1 when not eligible (then launch_group_decompress + launch_outlier_scatter)
+int launch_outlier_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                              const uint32_t *idx, const uint16_t *val, const int32_t *k_dev,
+                              int64_t k_cap, int64_t rows, int64_t cols, int64_t g, void *y, int ot);
+bool use_one_launch_outlier_decompress();
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot, const uint8_t *codes = nullptr,

@@ -498,3 +498,25 @@ def test_concurrent_streams_are_reentrant(torch_cuda):
             for a, b in zip(snapshot(slot, y), want):
                 assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
             assert int(slot.status[0]) == 0
+
+
+@pytest.mark.parametrize("shape,dtype_name", [((8192, 1024), "bfloat16"), ((1000, 40), "float32"),
+                                              ((2048, 4096), "float16"), ((333, 1024), "bfloat16")])
+def test_one_launch_outlier_decompress(torch_cuda, shape, dtype_name, monkeypatch):
+    """The opt-in single-launch outlier decompress (ADC_OUTLIER_DEQ1=1) writes
+    the same bytes as dequantise + scatter."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    rng = np.random.default_rng(shape[1])
+    x = rng.normal(size=shape).astype(np.float32)
+    hot = rng.choice(shape[1], max(2, shape[1] // 60), replace=False)
+    hot[1] = hot[0] ^ 1  # two flagged channels inside one 8-column unit
+    x[:, hot] *= 30
+    xt = torch.from_numpy(x).to(getattr(torch, dtype_name)).cuda()
+    ct = adc.compress(xt, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED))
+    for out in (torch.float32, torch.bfloat16):
+        monkeypatch.setenv("ADC_OUTLIER_DEQ1", "0")
+        want = adc.decompress(ct, out)
+        monkeypatch.setenv("ADC_OUTLIER_DEQ1", "1")
+        got = adc.decompress(ct, out)
+        assert torch.equal(got.view(torch.uint8), want.view(torch.uint8))
