@@ -137,7 +137,7 @@ __device__ __forceinline__ uint32_t mux_word(const uint32_t *w, int j) {
 // of g = EPL*L elements is owned by L adjacent lanes; U units per lane are
 // loaded before any is processed (memory-level parallelism).
 template <int DT, bool ASYM, int L, bool ZERO, int EPL, int U>
-__global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
+__global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 64) ? 3 : 4)
     group_quant_fast(const void *__restrict__ x, int64_t n_units, int64_t n_units_pad, FastDiv dc,
                      const uint8_t *__restrict__ zflag, OutlierSide side,
                      uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
@@ -160,23 +160,41 @@ __global__ void __launch_bounds__(kThreads, (EPL * U >= 64) ? 3 : 4)
     if (side.requant && __ldcg(side.requant) == 0u) return;
   }
   const int64_t step = n_ctas * kThreads * U;
-  for (int64_t base = cta * kThreads * U; base < n_units_pad; base += step) {
-    uint32_t w[U][NW];
-    uint2 zf[U][NC];
+  // asymmetric at 32 elements per lane: the next iteration's loads are issued
+  // before this one is processed (software pipeline), so every warp keeps a
+  // unit in flight while it computes (80 registers, 3 CTAs per SM)
+  constexpr bool PIPE = ASYM && EPL == 32;  // measured: asym 79.3 -> 77.5 us, sym / outlier slower
+  uint32_t wn[U][NW];
+  uint2 zfn[U][NC];
+  auto fetch = [&](int64_t b) {
 #pragma unroll
     for (int k = 0; k < U; ++k) {
-      const int64_t u = base + k * kThreads + threadIdx.x;
+      const int64_t u = b + k * kThreads + threadIdx.x;
 #pragma unroll
       for (int q = 0; q < NC; ++q) {
         uint4 v = make_uint4(0, 0, 0, 0);
         if (u < n_units) v = R::template load8<false>(x, u * EPL + 8 * q);
-        w[k][4 * q] = v.x;
-        w[k][4 * q + 1] = v.y;
-        w[k][4 * q + 2] = v.z;
-        w[k][4 * q + 3] = v.w;
-        if (ZERO) zf[k][q] = u < n_units ? zero_flags8(u * EPL + 8 * q, dc, zflag) : make_uint2(0, 0);
+        wn[k][4 * q] = v.x;
+        wn[k][4 * q + 1] = v.y;
+        wn[k][4 * q + 2] = v.z;
+        wn[k][4 * q + 3] = v.w;
+        if (ZERO) zfn[k][q] = u < n_units ? zero_flags8(u * EPL + 8 * q, dc, zflag) : make_uint2(0, 0);
       }
     }
+  };
+  if (PIPE && cta * kThreads * U < n_units_pad) fetch(cta * kThreads * U);
+  for (int64_t base = cta * kThreads * U; base < n_units_pad; base += step) {
+    if (!PIPE) fetch(base);
+    uint32_t w[U][NW];
+    uint2 zf[U][NC];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) w[k][i] = wn[k][i];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) zf[k][q] = zfn[k][q];
+    }
+    if (PIPE && base + step < n_units_pad) fetch(base + step);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
       const int64_t u = base + k * kThreads + threadIdx.x;
