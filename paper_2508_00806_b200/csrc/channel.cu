@@ -150,12 +150,38 @@ __global__ void __launch_bounds__(kThreads)
     channel_dequant(const uint8_t *__restrict__ codes, const uint16_t *__restrict__ scales,
                     int64_t rows, int64_t cols, void *__restrict__ y) {
   pdl_entry();
-  __shared__ uint32_t stage[kTileCols * kWordStride];
+  // all four sub-tiles' column-major code runs are staged with one barrier
+  // (2 x 16 B loads per thread in flight), then expanded without barriers
+  constexpr int kSubs = kBlockRows / kSubRows;
+  __shared__ uint32_t stage[kSubs][kTileCols * kWordStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 7, tyl = lane >> 3;
   const int rp = warp * 4 + tyl;
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTileCols + tx * 8;
   const bool col_live = c0 < cols;
+  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
+  {
+    uint4 v[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int item = threadIdx.x + q * kThreads;  // kSubs * kTileCols * 2 = 512 items
+      const int sub = item / (kTileCols * 2), within = item % (kTileCols * 2);
+      const int c = within >> 1, h = within & 1;
+      const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
+      const int64_t rs = row_begin + sub * kSubRows + 32 * h;
+      v[q] = (cg < cols && rs < rows) ? ld_stream16(codes + (cg * rows + rs) / 2) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int item = threadIdx.x + q * kThreads;
+      const int sub = item / (kTileCols * 2), within = item % (kTileCols * 2);
+      uint32_t *s = &stage[sub][(within >> 1) * kWordStride + 4 * (within & 1)];
+      s[0] = v[q].x;
+      s[1] = v[q].y;
+      s[2] = v[q].z;
+      s[3] = v[q].w;
+    }
+  }
   float sc[8];
   {
     uint4 v = col_live ? __ldg(reinterpret_cast<const uint4 *>(scales + c0)) : make_uint4(0, 0, 0, 0);
@@ -163,30 +189,15 @@ __global__ void __launch_bounds__(kThreads)
 #pragma unroll
     for (int j = 0; j < 8; ++j) sc[j] = h2f((w[j >> 1] >> ((j & 1) * 16)) & 0xffffu);
   }
-  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
-  for (int sub = 0; sub < kBlockRows / kSubRows; ++sub) {
-    const int64_t r0 = row_begin + sub * kSubRows;
-    if (r0 >= rows) break;
-    __syncthreads();
-    if (threadIdx.x < kTileCols * 2) {
-      const int c = threadIdx.x >> 1, h = threadIdx.x & 1;
-      const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
-      const int64_t rs = r0 + 32 * h;
-      uint4 v = make_uint4(0, 0, 0, 0);
-      if (cg < cols && rs < rows) v = ld_stream16(codes + (cg * rows + rs) / 2);
-      uint32_t *s = stage + c * kWordStride + 4 * h;
-      s[0] = v.x;
-      s[1] = v.y;
-      s[2] = v.z;
-      s[3] = v.w;
-    }
-    __syncthreads();
-    const int64_t r = r0 + 2 * rp;
+  __syncthreads();
+#pragma unroll
+  for (int sub = 0; sub < kSubs; ++sub) {
+    const int64_t r = row_begin + sub * kSubRows + 2 * rp;
     if (!col_live || r >= rows) continue;
     float va[8], vb[8];
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      const uint32_t word = stage[(tx * 8 + j) * kWordStride + warp];
+      const uint32_t word = stage[sub][(tx * 8 + j) * kWordStride + warp];
       const uint32_t byte = byte_of(word, tyl);
       va[j] = nib_code(byte, 0) * sc[j];
       vb[j] = nib_code(byte, 1) * sc[j];
