@@ -29,19 +29,66 @@ constexpr int kWordStride = 9;    // padded smem stride (words) per column
 // Byte `b` of word w.
 __device__ __forceinline__ uint32_t byte_of(uint32_t w, int b) { return (w >> (8 * b)) & 0xffu; }
 
+// Raw input words of 8 elements, converted to f16 words on use.
+template <int DT>
+struct ChRaw {
+  uint4 v;
+  __device__ __forceinline__ void load(const void *x, int64_t i) {
+    v = ld_stream16(static_cast<const char *>(x) + i * 2);
+  }
+  __device__ __forceinline__ void zero() { v = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ uint4 f16() const {
+    if (DT == ADC_BF16) return make_uint4(bf2_to_h2(v.x), bf2_to_h2(v.y), bf2_to_h2(v.z), bf2_to_h2(v.w));
+    return v;
+  }
+};
+template <>
+struct ChRaw<ADC_F32> {
+  uint4 a, b;
+  __device__ __forceinline__ void load(const void *x, int64_t i) {
+    const char *p = static_cast<const char *>(x) + i * 4;
+    a = ld_stream16(p);
+    b = ld_stream16(p + 16);
+  }
+  __device__ __forceinline__ void zero() { a = b = make_uint4(0, 0, 0, 0); }
+  __device__ __forceinline__ uint4 f16() const {
+    return make_uint4(f32x2_to_h2(__uint_as_float(a.x), __uint_as_float(a.y)),
+                      f32x2_to_h2(__uint_as_float(a.z), __uint_as_float(a.w)),
+                      f32x2_to_h2(__uint_as_float(b.x), __uint_as_float(b.y)),
+                      f32x2_to_h2(__uint_as_float(b.z), __uint_as_float(b.w)));
+  }
+};
+
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
     channel_quant(const void *__restrict__ x, int64_t rows, int64_t cols,
                   const uint32_t *__restrict__ colmax, uint8_t *__restrict__ codes,
                   uint16_t *__restrict__ scales) {
   pdl_entry();
-  __shared__ uint32_t stage[kTileCols * kWordStride];
+  // all four sub-tiles: their rows are loaded up front (8 x 16 B in flight per
+  // thread, issued before the scales are derived), quantised into four
+  // separate shared-memory stages, and written with one barrier
+  constexpr int kSubs = kBlockRows / kSubRows;
+  __shared__ uint32_t stage[kSubs][kTileCols * kWordStride];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 7;         // column unit inside the tile
   const int tyl = lane >> 3;       // row pair inside the warp (0..3)
   const int rp = warp * 4 + tyl;   // row pair inside the sub-tile (0..31)
   const int64_t c0 = static_cast<int64_t>(blockIdx.x) * kTileCols + tx * 8;
   const bool col_live = c0 < cols;
+  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
+  ChRaw<DT> ra[kSubs], rb[kSubs];
+#pragma unroll
+  for (int sub = 0; sub < kSubs; ++sub) {
+    const int64_t r = row_begin + sub * kSubRows + 2 * rp;
+    if (col_live && r < rows) {  // rows % 32 == 0 => r+1 < rows too
+      ra[sub].load(x, r * cols + c0);
+      rb[sub].load(x, (r + 1) * cols + c0);
+    } else {
+      ra[sub].zero();
+      rb[sub].zero();
+    }
+  }
 
   // Per-column quantisation constants for this thread's 8 columns.
   float qs[8], qi[8];
@@ -64,17 +111,9 @@ __global__ void __launch_bounds__(kThreads)
     }
   }
 
-  const int64_t row_begin = static_cast<int64_t>(blockIdx.y) * kBlockRows;
-  for (int sub = 0; sub < kBlockRows / kSubRows; ++sub) {
-    const int64_t r0 = row_begin + sub * kSubRows;
-    if (r0 >= rows) break;
-    const int64_t r = r0 + 2 * rp;
-    const bool live = col_live && r < rows;  // rows % 32 == 0 => r+1 < rows too
-    uint4 ha = make_uint4(0, 0, 0, 0), hb = make_uint4(0, 0, 0, 0);
-    if (live) {
-      ha = Loader<DT>::template load8<false>(x, r * cols + c0);
-      hb = Loader<DT>::template load8<false>(x, (r + 1) * cols + c0);
-    }
+#pragma unroll
+  for (int sub = 0; sub < kSubs; ++sub) {
+    const uint4 ha = ra[sub].f16(), hb = rb[sub].f16();
     // byte j = code(row r, col j) | code(row r+1, col j) << 4
     uint32_t lo = 0, hi = 0;
     if (fast) {
@@ -128,19 +167,20 @@ __global__ void __launch_bounds__(kThreads)
       tlo |= byte_of(plo, tyl) << (8 * t);
       thi |= byte_of(phi, tyl) << (8 * t);
     }
-    __syncthreads();  // previous sub-tile's stage has been drained
-    stage[(tx * 8 + tyl) * kWordStride + warp] = tlo;
-    stage[(tx * 8 + 4 + tyl) * kWordStride + warp] = thi;
-    __syncthreads();
-    if (threadIdx.x < kTileCols * 2) {
-      const int c = threadIdx.x >> 1, h = threadIdx.x & 1;
-      const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
-      const int64_t rs = r0 + 32 * h;
-      if (cg < cols && rs < rows) {
-        const uint32_t *s = stage + c * kWordStride + 4 * h;
-        uint4 v = make_uint4(s[0], s[1], s[2], s[3]);
-        st_stream16(codes + (cg * rows + rs) / 2, v);
-      }
+    stage[sub][(tx * 8 + tyl) * kWordStride + warp] = tlo;
+    stage[sub][(tx * 8 + 4 + tyl) * kWordStride + warp] = thi;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {  // kSubs * kTileCols * 2 = 512 column runs of 16 B
+    const int item = threadIdx.x + q * kThreads;
+    const int sub = item / (kTileCols * 2), within = item % (kTileCols * 2);
+    const int c = within >> 1, h = within & 1;
+    const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
+    const int64_t rs = row_begin + sub * kSubRows + 32 * h;
+    if (cg < cols && rs < rows) {
+      const uint32_t *sp = &stage[sub][c * kWordStride + 4 * h];
+      st_stream16(codes + (cg * rows + rs) / 2, make_uint4(sp[0], sp[1], sp[2], sp[3]));
     }
   }
 }
