@@ -30,11 +30,13 @@ __device__ __forceinline__ uint32_t fastdiv(uint32_t n, const FastDiv &f) {
 // gather CTAs (OutlierSide), not from here: storing them here scattered
 // 2-byte writes across k rows of the buffer and stalled the quantiser on the
 // store queue (ncu, r1).
+// e is a multiple of 8 and cols % 8 == 0, so the column is 8 * ((e / 8) mod
+// (cols / 8)): dc divides by cols / 8, exact for e / 8 < 2^31 (n < 2^34).
 __device__ __forceinline__ uint2 zero_flags8(int64_t e, const FastDiv &dc,
                                              const uint8_t *__restrict__ zflag) {
-  const uint32_t r = fastdiv(static_cast<uint32_t>(e), dc);
-  const uint32_t c = static_cast<uint32_t>(e) - r * dc.d;
-  return __ldg(reinterpret_cast<const uint2 *>(zflag + c));
+  const uint32_t e8 = static_cast<uint32_t>(e >> 3);
+  const uint32_t c8 = e8 - fastdiv(e8, dc) * dc.d;
+  return __ldg(reinterpret_cast<const uint2 *>(zflag) + c8);
 }
 // Side-buffer gather for the outlier-separated scheme (codec.py:331-341):
 // val[rank][r] = f16(x[r, idx[rank]]).  Run by the first n_gather CTAs of the
@@ -748,12 +750,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
   const int64_t n = rows * cols;
   const bool pc = (g == 0);
   const bool zero = zero_flag != nullptr;
-  const bool zero_ok = !zero || (cols % 8 == 0 && n < (1ll << 31));
-  const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols > 0 ? cols : 1));
+  const bool zero_ok = !zero || (cols % 8 == 0 && n / 8 < (1ll << 31));
+  const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols >= 8 ? cols / 8 : 1));  // zero_flags8
   OutlierSide side = outlier_side(c, idx, k_dev, zero ? k_cap : 0, rows, cols, outl_val);
   side.requant = zero ? requant : nullptr;
   int L = pc ? 0 : lanes_for_group(g, 8);
-  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok) {
+  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok &&
+      (!zero || n < (1ll << 31))) {
     const int rc = launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, codes,
                                              scales, offsets, err);
     if (rc || !zero) return rc;

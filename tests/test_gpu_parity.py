@@ -426,6 +426,37 @@ def test_outlier_decompress_sector_patch_large_outputs(torch_cuda, rows):
     assert torch.equal(y32.view(torch.int32), ref.view(torch.int32))
 
 
+def test_outlier_separated_at_2_31_elements(torch_cuda):
+    """2^31 elements (4 GB bf16) stays exact on the fast quantiser (the
+    channel index of the zeroing step is taken on 8-element units).  The
+    input is a [256, 4096] block tiled 2048 times down the rows: a power-of-2
+    repetition scales every column sum, the mean and the std exactly, so the
+    flagged set, codes, scales and side values are the block's, tiled."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    rows0, cols, reps = 256, 4096, 2048
+    g = torch.Generator(device="cuda").manual_seed(31)
+    blk = torch.randn(rows0, cols, device="cuda", generator=g)
+    hot = torch.randperm(cols, generator=g, device="cuda")[:29]
+    blk[:, hot] *= 40
+    blk = blk.to(torch.bfloat16)
+    spec = adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED)
+    small = adc.compress(blk, spec)
+    x = blk.repeat(reps, 1)
+    assert x.numel() == 1 << 31
+    big = adc.compress(x, spec)
+    del x
+    assert torch.equal(big.outlier_indices, small.outlier_indices)
+    assert small.outlier_indices.numel() == 29
+    assert torch.equal(big.packed_codes.view(reps, -1), small.packed_codes.view(1, -1).expand(reps, -1))
+    assert torch.equal(big.scales.view(reps, -1), small.scales.view(1, -1).expand(reps, -1))
+    k = small.outlier_indices.numel()
+    assert torch.equal(big.outlier_values.view(k, reps, rows0), small.outlier_values.view(k, 1, rows0).expand(k, reps, rows0))
+    y = adc.decompress(big, torch.bfloat16)
+    y0 = adc.decompress(small, torch.bfloat16)
+    assert torch.equal(y.view(reps, rows0, cols).view(torch.int16), y0.view(1, rows0, cols).expand(reps, rows0, cols).view(torch.int16))
+
+
 @pytest.mark.parametrize("scheme,group,shape", [
     (cases.SYM, 128, (300, 70)), (cases.ASYM, 128, (256, 768)), (cases.OUTL, 128, (512, 1024)),
     (cases.SYM, 0, (64, 96)), (cases.MASK, 0, (33, 17)), (cases.ASYM, 7, (5, 11)), (cases.OUTL, 64, (1000, 40))])
