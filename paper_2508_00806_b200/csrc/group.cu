@@ -50,6 +50,7 @@ struct OutlierSide {
   uint16_t *val;
   int n_gather;  // leading CTAs that gather (0: none)
   const uint32_t *requant;  // non-null: quantise only if *requant != 0 (speculation missed)
+  int tail_gather;  // 1: every quantising CTA gathers after its units (no leading gather CTAs)
 };
 constexpr int kGatherRanks = 8;
 
@@ -159,7 +160,10 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
     n_ctas -= side.n_gather;
     // the speculative column-statistics kernel already wrote codes / scales
     // with the predicted channel set; re-quantise only if it missed
-    if (side.requant && __ldcg(side.requant) == 0u) return;
+    if (side.requant && __ldcg(side.requant) == 0u) {
+      if (side.tail_gather) gather_side<DT>(x, side, cta, n_ctas);
+      return;
+    }
   }
   const int64_t step = n_ctas * kThreads * U;
   // asymmetric at 32 elements per lane: the next iteration's loads are issued
@@ -366,6 +370,7 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
       }
     }
   }
+  if (ZERO && side.tail_gather) gather_side<DT>(x, side, cta, n_ctas);
 }
 
 template <int OT, bool ASYM, int L, int EPL, int U>
@@ -732,12 +737,26 @@ constexpr int kUnroll = 2;
 constexpr int kU32 = 1;  // units in flight per lane at 32 elements per lane
 constexpr int kUD = 4;   // units in flight per lane in the 8-element dequantiser
 
-// Gather work: (k_cap / 8) rank blocks x (rows / 256) row blocks, at most
-// one CTA per SM (the gather is latency-bound and short).
+// Gather work: (k_cap / 8) rank blocks x (rows / 256) row blocks, either up
+// to one leading gather CTA per SM, or taken by the quantising CTAs after
+// their units ("tail").  Leading CTAs hold slots the one-wave quantiser grid
+// counts on, so its last CTAs start late: measured 147 -> 143 us at
+// [131072, 1024] with the tail, but 19.5 -> 20.1 us at [8192, 1024] (the
+// tail adds a dependent gather round trip to short kernels).  Default: tail
+// from 2^26 elements; ADC_GATHER_TAIL=0/1 forces either.
+static bool use_tail_gather(int64_t n) {
+  const char *e = getenv("ADC_GATHER_TAIL");
+  return e ? atoi(e) != 0 : n >= (int64_t{1} << 26);
+}
 static OutlierSide outlier_side(const Ctx &c, const uint32_t *idx, const int32_t *k_dev,
-                                int64_t k_cap, int64_t rows, int64_t cols, uint16_t *val) {
-  OutlierSide o{idx, k_dev, k_cap, rows, cols, val, 0, nullptr};
+                                int64_t k_cap, int64_t rows, int64_t cols, uint16_t *val,
+                                bool tail_ok = true) {
+  OutlierSide o{idx, k_dev, k_cap, rows, cols, val, 0, nullptr, 0};
   if (k_cap <= 0 || !val || !idx || !k_dev) return o;
+  if (tail_ok && use_tail_gather(rows * cols)) {
+    o.tail_gather = 1;
+    return o;
+  }
   const int64_t items = ((rows + kThreads - 1) / kThreads) * ((k_cap + kGatherRanks - 1) / kGatherRanks);
   o.n_gather = static_cast<int>(items < c.num_sms ? items : c.num_sms);
   return o;
@@ -848,7 +867,7 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
 int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *idx,
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                           uint16_t *outl_val) {
-  const OutlierSide side = outlier_side(c, idx, k_dev, k_cap, rows, cols, outl_val);
+  const OutlierSide side = outlier_side(c, idx, k_dev, k_cap, rows, cols, outl_val, false);
   if (side.n_gather == 0) return 0;
   ADC_DT_SWITCH(dt, DT, launch_k(outlier_gather<DT>, side.n_gather, kThreads, 0, c.stream, x, side),
                 note_launches(1));

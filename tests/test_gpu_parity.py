@@ -426,6 +426,24 @@ def test_outlier_decompress_sector_patch_large_outputs(torch_cuda, rows):
     assert torch.equal(y32.view(torch.int32), ref.view(torch.int32))
 
 
+@pytest.mark.parametrize("shape,dtype_name", [((512, 1024), "bfloat16"), ((1000, 40), "float32"),
+                                              ((257, 4096), "float16")])
+def test_outlier_gather_modes_vs_oracle(torch_cuda, shape, dtype_name, monkeypatch):
+    """The side-buffer gather by leading CTAs (ADC_GATHER_TAIL=0) and by the
+    quantising CTAs after their units (=1) both match the oracle."""
+    torch = torch_cuda
+    rng = np.random.default_rng(shape[0])
+    x = rng.normal(size=shape).astype(np.float32)
+    x[:, rng.choice(shape[1], max(2, shape[1] // 50), replace=False)] *= 30
+    xt = torch.from_numpy(x).to(getattr(torch, dtype_name))
+    want = oracle_run(xt.to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+    assert isinstance(want[0], dict) and want[0]["idx"] is not None and len(want[0]["idx"]) >= 2
+    for mode in ("0", "1"):
+        monkeypatch.setenv("ADC_GATHER_TAIL", mode)
+        got = device_run(xt, cases.OUTL, 128, 3.0)
+        assert cases.norm_digest(*got) == cases.norm_digest(*want), mode
+
+
 def test_outlier_separated_at_2_31_elements(torch_cuda):
     """2^31 elements (4 GB bf16) stays exact on the fast quantiser (the
     channel index of the zeroing step is taken on 8-element units).  The
