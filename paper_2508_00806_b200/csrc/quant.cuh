@@ -24,15 +24,16 @@ __device__ __forceinline__ uint32_t warp_min_u2(uint32_t v) {
 
 // Zero the flagged channels of 8 consecutive elements of one row: byte j of
 // f (0/1) is the flag of element j; 16-bit lane j is kept iff its flag is 0.
+// Branch-free (a per-segment branch executed for whole warps anyway, ~23
+// instructions per 8 elements in ncu): flags * 0xFF turns each 0/1 byte into
+// 0x00/0xFF, one PRMT doubles two of them into a 16-bit-lane mask, one LOP3
+// clears the lanes -- 10 instructions per 8 elements.
 __device__ __forceinline__ void zero_apply8(uint32_t *w, uint2 f) {
-  if ((f.x | f.y) != 0) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t fw = i < 2 ? f.x : f.y;
-      const uint32_t lo = (fw >> (16 * (i & 1))) & 0xffu, hi = (fw >> (16 * (i & 1) + 8)) & 0xffu;
-      w[i] &= (lo ? 0xffff0000u : 0xffffffffu) & (hi ? 0x0000ffffu : 0xffffffffu);
-    }
-  }
+  const uint32_t mx = f.x * 0xffu, my = f.y * 0xffu;
+  w[0] &= ~__byte_perm(mx, 0u, 0x1100);
+  w[1] &= ~__byte_perm(mx, 0u, 0x3322);
+  w[2] &= ~__byte_perm(my, 0u, 0x1100);
+  w[3] &= ~__byte_perm(my, 0u, 0x3322);
 }
 
 __device__ __forceinline__ float lo_f(uint32_t w) {
