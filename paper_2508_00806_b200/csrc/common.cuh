@@ -328,6 +328,22 @@ __device__ __forceinline__ uint32_t asym_tbits(float h, const QParams &q) {
   return __float_as_uint(t);
 }
 
+// Pack 8 UNCLIPPED t-bits into one word of 4-bit two's-complement codes,
+// element 0 lowest, saturating to [-8, 7] on the way (codec.py:231 clip, then
+// :199-203 nibble order): code = t - bits(kMagic8) as s32, two codes per
+// I2IP.S4.S32.SAT (cvt.pack.sat.s4), the earlier pairs shifted up by 8 bits
+// through the third operand.  4 packs + 8 subtracts replace the per-element
+// clips and the IMAD/PRMT packing.  Valid while |r| < 2^22 (magic-add range).
+__device__ __forceinline__ uint32_t pack8_tbits_sat(const uint32_t *t) {
+  constexpr uint32_t K = 0x4B400008u;
+  uint32_t d;
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, 0;" : "=r"(d) : "r"(t[7] - K), "r"(t[6] - K));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(t[5] - K), "r"(t[4] - K), "r"(d));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(t[3] - K), "r"(t[2] - K), "r"(d));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(t[1] - K), "r"(t[0] - K), "r"(d));
+  return d;
+}
+
 // Pack 8 t-bits (elements 0..7) into one word of nibbles, element 0 lowest
 // (codec.py:199-203): pairs by IMAD (hi*16 + lo keeps both nibbles in the low
 // byte), bytes gathered by PRMT, the +8 offset removed by one XOR.

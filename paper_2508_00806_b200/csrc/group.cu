@@ -210,7 +210,6 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
         for (int q = 0; q < NC; ++q) zero_apply8(&w[k][4 * q], zf[k][q]);
       }
       uint16_t s_bits, o_bits = 0;
-      uint32_t lo_bits = 0;  // asymmetric: the group minimum (f16 bits)
       bool bad, native = true;
       if (ASYM) {
         // packed max/min (NaN-propagating) in the input's own 16-bit format
@@ -240,7 +239,6 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
         }
         bad = ((hi & 0x7fffu) >= 0x7c00u) || ((lo & 0x7fffu) >= 0x7c00u);
         asym_params(hi, lo, o_bits, s_bits);
-        lo_bits = lo;
       } else {
         uint32_t m = 0;
         if (act) {
@@ -276,24 +274,18 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
         // within that margin (doubled) of a half-integer are redone exactly.
         const float oi = q.o * q.inv;
         const float thr = 0.5f - (0x1p-17f + fabsf(oi) * 0x1p-22f + (BF ? 0x1p-25f * q.inv : 0.f));
-        // the lower clip only matters for degenerate groups whose minimum
-        // quotient can fall below -8.5 (f16 rounding of a large offset)
-        const bool clip_lo = fmaf(h2f(lo_bits), q.inv, -oi) < -8.f;
+        // no clips here: the codes saturate to [-8, 7] when packed
+        // (pack8_tbits_sat); an unclipped quotient beyond the range only
+        // rounds to a code the saturation maps to the clipped one, and a
+        // near-tie flagged there is redone exactly like any other
         // two elements per FFMA2 / FADD2; rounding residuals |e| beyond thr
         // mark the elements redone exactly (frequent for bf16 data, whose
         // coarse mantissas make exact half-integer quotients common)
         const uint64_t inv2 = f2_pack(q.inv, q.inv), noi2 = f2_pack(-oi, -oi);
         const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
-        auto pair = [&](int i, bool lo_clip) {
-          float rl, rh;
-          f2_unpack(f2_fma(f2_pack(R::lo(w[k][i]), R::hi(w[k][i])), inv2, noi2), rl, rh);
-          rl = fminf(rl, 7.f);
-          rh = fminf(rh, 7.f);
-          if (lo_clip) {
-            rl = fmaxf(rl, -8.f);
-            rh = fmaxf(rh, -8.f);
-          }
-          const uint64_t r2 = f2_pack(rl, rh);
+#pragma unroll
+        for (int i = 0; i < NW; ++i) {
+          const uint64_t r2 = f2_fma(f2_pack(R::lo(w[k][i]), R::hi(w[k][i])), inv2, noi2);
           const uint64_t tv2 = f2_add(r2, mg2);
           float el, eh, tl, th;
           f2_unpack(f2_sub(r2, f2_sub(tv2, mg2)), el, eh);
@@ -302,13 +294,6 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
           fix |= (fabsf(eh) > thr ? 1u : 0u) << (2 * i + 1);
           t[2 * i] = __float_as_uint(tl);
           t[2 * i + 1] = __float_as_uint(th);
-        };
-        if (__any_sync(__activemask(), clip_lo)) {  // degenerate groups only
-#pragma unroll
-          for (int i = 0; i < NW; ++i) pair(i, true);
-        } else {
-#pragma unroll
-          for (int i = 0; i < NW; ++i) pair(i, false);
         }
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
@@ -339,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
       }
       uint32_t cw[NC];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) cw[q] = pack8_tbits(t + 8 * q);
+      for (int q = 0; q < NC; ++q) cw[q] = ASYM ? pack8_tbits_sat(t + 8 * q) : pack8_tbits(t + 8 * q);
       if (ASYM) {
         const float sc = h2f(s_bits), so = h2f(o_bits);
         const float scd = sc == 0.f ? 1.f : sc, inv = rcp_approx(scd);
