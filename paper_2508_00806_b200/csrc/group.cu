@@ -298,7 +298,7 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
           // correctly rounded h/s two lanes per FMUL2 / FFMA2 (Markstein),
-          // RNE by the magic add, clip to 7 on the bit pattern
+          // RNE by the magic add, clip to 7 in the saturating pack
           const float sc = h2f(s_bits), inv = rcp_approx(sc);
           const uint64_t inv2 = f2_pack(inv, inv), ns2 = f2_pack(-sc, -sc), mg2 = f2_pack(kMagic8, kMagic8);
 #pragma unroll
@@ -308,8 +308,8 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
             const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
             float tl, th;
             f2_unpack(f2_add(r1, mg2), tl, th);
-            t[2 * i] = min(__float_as_uint(tl), 0x4B40000Fu);
-            t[2 * i + 1] = min(__float_as_uint(th), 0x4B40000Fu);
+            t[2 * i] = __float_as_uint(tl);  // upper clip: saturating pack
+            t[2 * i + 1] = __float_as_uint(th);
           }
         } else {
           const float s0 = h2f(s_bits), sc = s0 == 0.f ? 1.f : s0, inv = rcp_approx(sc);
@@ -324,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
       }
       uint32_t cw[NC];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) cw[q] = ASYM ? pack8_tbits_sat(t + 8 * q) : pack8_tbits(t + 8 * q);
+      for (int q = 0; q < NC; ++q) cw[q] = pack8_tbits_sat(t + 8 * q);
       if (ASYM) {
         const float sc = h2f(s_bits), so = h2f(o_bits);
         const float scd = sc == 0.f ? 1.f : sc, inv = rcp_approx(scd);
