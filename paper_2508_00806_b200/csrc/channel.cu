@@ -119,10 +119,11 @@ __global__ void __launch_bounds__(kThreads)
     if (fast) {
       // rows r and r+1 of column j share its scale: one FMUL2 / two FFMA2
       // give both correctly rounded quotients, the magic add rounds them,
-      // one IMAD joins the two nibbles into the byte (see pack8_tbits)
+      // one saturating I2IP clips both and joins them into the byte, chained
+      // four bytes per word (see pack8_tbits_sat)
       const uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w}, wb[4] = {hb.x, hb.y, hb.z, hb.w};
       const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
-      uint32_t by[8];
+      uint32_t ta_[8], tb_[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t sh = (j & 1) * 16;
@@ -132,10 +133,11 @@ __global__ void __launch_bounds__(kThreads)
         const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
         float ta, tb;
         f2_unpack(f2_add(r1, mg2), ta, tb);
-        by[j] = min(__float_as_uint(tb), 0x4B40000Fu) * 16u + min(__float_as_uint(ta), 0x4B40000Fu);
+        ta_[j] = __float_as_uint(ta) - 0x4B400008u;  // s32 codes
+        tb_[j] = __float_as_uint(tb) - 0x4B400008u;
       }
-      lo = __byte_perm(__byte_perm(by[0], by[1], 0x0040), __byte_perm(by[2], by[3], 0x0040), 0x5410) ^ 0x88888888u;
-      hi = __byte_perm(__byte_perm(by[4], by[5], 0x0040), __byte_perm(by[6], by[7], 0x0040), 0x5410) ^ 0x88888888u;
+      lo = pack4_pairs_sat(ta_, tb_);
+      hi = pack4_pairs_sat(ta_ + 4, tb_ + 4);
     } else {
       uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w};
       uint32_t wb[4] = {hb.x, hb.y, hb.z, hb.w};

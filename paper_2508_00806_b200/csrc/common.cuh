@@ -344,6 +344,17 @@ __device__ __forceinline__ uint32_t pack8_tbits_sat(const uint32_t *t) {
   return d;
 }
 
+// Four bytes (a[j] low nibble, b[j] high nibble, byte j) from s32 codes,
+// saturated to [-8, 7]: one I2IP.S4.S32.SAT per byte.
+__device__ __forceinline__ uint32_t pack4_pairs_sat(const uint32_t *a, const uint32_t *b) {
+  uint32_t d;
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, 0;" : "=r"(d) : "r"(b[3]), "r"(a[3]));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b[2]), "r"(a[2]), "r"(d));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b[1]), "r"(a[1]), "r"(d));
+  asm("cvt.pack.sat.s4.s32.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(b[0]), "r"(a[0]), "r"(d));
+  return d;
+}
+
 // Pack 8 t-bits (elements 0..7) into one word of nibbles, element 0 lowest
 // (codec.py:199-203): pairs by IMAD (hi*16 + lo keeps both nibbles in the low
 // byte), bytes gathered by PRMT, the +8 offset removed by one XOR.
