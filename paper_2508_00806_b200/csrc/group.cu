@@ -283,18 +283,28 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
         // coarse mantissas make exact half-integer quotients common)
         const uint64_t inv2 = f2_pack(q.inv, q.inv), noi2 = f2_pack(-oi, -oi);
         const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
+        // the test |e| > thr as the sign of fma(e, e, -t2) (exact sign; t2 <
+        // thr^2, so every near tie is caught, plus at most a few elements
+        // just inside the margin, which the exact pass recomputes): one
+        // FFMA2 per pair on the FMA pipe, then one funnel shift per element
+        // pushes the sign into the mask (bit-reversed and inverted once)
+        const float t2 = thr * thr * (1.f - 0x1p-20f);
+        const uint64_t nt2 = f2_pack(-t2, -t2);
+        uint32_t signs = 0;
 #pragma unroll
         for (int i = 0; i < NW; ++i) {
           const uint64_t r2 = f2_fma(f2_pack(R::lo(w[k][i]), R::hi(w[k][i])), inv2, noi2);
           const uint64_t tv2 = f2_add(r2, mg2);
-          float el, eh, tl, th;
-          f2_unpack(f2_sub(r2, f2_sub(tv2, mg2)), el, eh);
+          const uint64_t e2 = f2_sub(r2, f2_sub(tv2, mg2));
+          float dl, dh, tl, th;
+          f2_unpack(f2_fma(e2, e2, nt2), dl, dh);
+          signs = __funnelshift_l(__float_as_uint(dl), signs, 1);
+          signs = __funnelshift_l(__float_as_uint(dh), signs, 1);
           f2_unpack(tv2, tl, th);
-          fix |= (fabsf(el) > thr ? 1u : 0u) << (2 * i);
-          fix |= (fabsf(eh) > thr ? 1u : 0u) << (2 * i + 1);
           t[2 * i] = __float_as_uint(tl);
           t[2 * i + 1] = __float_as_uint(th);
         }
+        fix = ~__brev(signs) >> (32 - EPL);
       } else if (!BF || native) {
         if (s_bits >= 0x0400u) {  // normal scale: upper clip only
           // correctly rounded h/s two lanes per FMUL2 / FFMA2 (Markstein),
