@@ -431,6 +431,13 @@ struct Storer<ADC_F16> {
   }
 };
 
+// gpu-scope acquire-release fetch-add (arrival counters)
+__device__ __forceinline__ uint32_t atom_add_acq_rel_gpu(uint32_t *p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // ---------------------------------------------------------------------------
 // mbarrier + bulk-copy (TMA engine, 1-D) pipeline primitives
 // ---------------------------------------------------------------------------

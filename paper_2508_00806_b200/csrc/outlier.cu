@@ -164,14 +164,16 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
       if (c < cols && v != 0u) atomicMax(a.macc + c, v);
     }
   }
-  // ---- stage B: the last CTA finalises
-  __threadfence();
+  // ---- stage B: the last CTA finalises.  Arrival: CTA barrier, then one
+  // acq_rel atomic by thread 0 -- release publishes every thread's column
+  // atomics (barrier + cumulative release, the split-K semaphore pattern),
+  // acquire lets the last CTA (after its barrier) read all of them; no
+  // per-thread fence
   __syncthreads();
   if (threadIdx.x == 0)
-    s_last = atomicAdd(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
+    s_last = atom_add_acq_rel_gpu(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!s_last) return;
-  __threadfence();
   // move the accumulators out (4 columns per thread per round trip) and reset them
   const bool s_smem = SUM && cols <= kSmemSumCols;
   double *s_S = reinterpret_cast<double *>(s_buf);
