@@ -965,16 +965,16 @@ int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *va
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot, const uint8_t *codes, const uint16_t *scales, int64_t g) {
   if (k_cap <= 0) return 0;
-  // whole-sector patches when the output is too large to still sit in L2
-  // (then a 2-byte scatter pays a DRAM read-modify-write per element;
-  // measured 127.7 -> 105.9 us for [131072,1024] bf16, k = 11) and the codes
-  // are row-major groups that never straddle a 32-byte output sector; small
-  // outputs keep the scatter (one dependent load instead of two: 8.3 vs
-  // 12.9 us at [8192,1024])
+  // whole-sector patches when the output is large (then a 2-byte scatter
+  // pays a read-modify-write per element; measured 127.7 -> 105.9 us for
+  // [131072,1024] bf16, k = 11; 30.5 -> 29.0 us at [8192,4096], 64 MB) and
+  // the codes are row-major groups that never straddle a 32-byte output
+  // sector; smaller outputs keep the scatter (one dependent load instead of
+  // two: 8.3 vs 12.9 us at [8192,1024], 23.9 vs 25.8 us at [8192,3072])
   const int se = ot == ADC_F32 ? 8 : 16;
   const int L = codes && scales ? lanes_for_group(g, 8) : 0;
   const int64_t out_bytes = rows * cols * (ot == ADC_F32 ? 4 : 2);
-  if (L > 0 && out_bytes > (128ll << 20) && g % se == 0 && cols % se == 0 && aligned(y, 32) &&
+  if (L > 0 && out_bytes >= (64ll << 20) && g % se == 0 && cols % se == 0 && aligned(y, 32) &&
       aligned(codes, 4)) {
     const int64_t gx = std::max<int64_t>(1, std::min<int64_t>((rows + 4 * kThreads - 1) / (4 * kThreads), 64));
     const int64_t gy = std::max<int64_t>(1, std::min<int64_t>(k_cap, std::max<int64_t>(1, 8 * c.num_sms / gx)));
