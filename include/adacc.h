@@ -109,6 +109,9 @@ ADC_API int adc_set_option(const char *key, int value);
  * deltas at the end of each phase) to host memory.  Returns the count copied.
  */
 ADC_API int adc_debug_trace(unsigned long long *out, int n);
+/* Same for the single-pass outlier-separated kernel (adc_set_option("k4_trace", 1)):
+ * 16 u64 per CTA (globaltimer at entry, clock64 deltas at phase ends). */
+ADC_API int adc_debug_trace_k4(unsigned long long *out, int n);
 
 /*
  * Closed-form payload size; replaces packed_payload_bytes (codec.py:133-145).

@@ -72,7 +72,7 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   };
   Workspace w;
   const int64_t nodes = node_capacity(cols);
-  w.counters = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * 4));
+  w.counters = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * 8));
   w.colsum = reinterpret_cast<double *>(take(sizeof(double) * cols));
   w.colmax = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.flag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
@@ -81,6 +81,7 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   w.node_left = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
   w.acc = reinterpret_cast<double *>(take(sizeof(double) * cols));
+  w.k4acc = reinterpret_cast<double *>(take(sizeof(double) * 2 * cols));
   w.macc = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.pflag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
   w.bytes = off;
@@ -127,8 +128,12 @@ int adc_set_option(const char *key, int value) {
     set_fused_trace(value);
     return ADC_OK;
   }
-  if (k == "outlier_path") {  // 1: single-launch fused kernel (default), 2: colreduce + quantiser
-    set_fused_outlier(value == 1);
+  if (k == "outlier_path") {  // 0: colreduce + quantiser, 1: single pass (default), 2: single pass + speculation
+    set_k4_mode(value);
+    return ADC_OK;
+  }
+  if (k == "k4_trace") {  // record phase timestamps of the single-pass kernel (adc_debug_trace_k4)
+    set_k4_trace(value);
     return ADC_OK;
   }
   return fail(ADC_EINVAL, "unknown option");
@@ -137,6 +142,12 @@ int adc_set_option(const char *key, int value) {
 int adc_debug_trace(unsigned long long *out, int n) {
   if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
   const int r = read_fused_trace(out, n);
+  return r < 0 ? fail(ADC_ECUDA, "trace copy failed") : r;
+}
+
+int adc_debug_trace_k4(unsigned long long *out, int n) {
+  if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
+  const int r = read_k4_trace(out, n);
   return r < 0 ? fail(ADC_ECUDA, "trace copy failed") : r;
 }
 
@@ -201,6 +212,9 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
       return fail(ADC_EWORKSPACE, "workspace too small");
     Workspace ws;
     workspace_layout(cols, &ws, workspace);
+    if (launch_outlier_k4(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws, codes, scales,
+                          outlier_idx, outlier_val, k_out, err_word))
+      return check_launch("outlier_single_pass");
     if (launch_outlier_fused(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
                              codes, scales, outlier_idx, outlier_val, k_out, err_word))
       return check_launch("outlier_fused");

@@ -59,8 +59,9 @@ struct Workspace {
   uint32_t *colmax;      // cols       column abs-max f16 bits (per-channel)
   uint8_t *flag;         // cols + 8   outlier flags
   double *acc;           // cols       f64 atomic column-sum accumulators (zero at rest)
+  double *k4acc;         // 2 x cols   single-pass kernel's bulk-reduction targets (double-buffered)
   uint32_t *macc;        // cols       u32 atomic column-max accumulators (zero at rest)
-  uint32_t *counters;    // 4          arrival counters (zero at rest)
+  uint32_t *counters;    // 8          arrival counters ([0..3] colreduce / fused, [4..6] k4; zero at rest but [5])
   uint8_t *pflag;        // cols + 8   previous outlier flags (fused kernel's prediction; any
                          //            content is valid, zero-fill = "no outliers")
   int32_t *node_lo;      // pairwise-tree nodes (used when cols > 16384)
@@ -113,6 +114,18 @@ int launch_outlier_fused(const Ctx &c, const void *x, int dt, int64_t rows, int6
                          int64_t g, double thr, int64_t k_cap, const Workspace &ws,
                          uint8_t *codes, uint16_t *scales, uint32_t *idx, uint16_t *val,
                          int32_t *k_out, uint32_t *err);
+// single-pass outlier-separated compress (k4.cu): returns 1 if it ran, 0 if
+// the shape is not eligible or the path is switched off (ADC_OUTLIER_PATH=2 /
+// adc_set_option("outlier_path", 0)); mode 2 (ADC_OUTLIER_PATH=s) speculates
+// with the previous call's channel set.
+int launch_outlier_k4(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols, int64_t g,
+                      double thr, int64_t k_cap, const Workspace &ws, uint8_t *codes,
+                      uint16_t *scales, uint32_t *idx, uint16_t *val, int32_t *k_out,
+                      uint32_t *err);
+int k4_mode();
+void set_k4_mode(int v);
+void set_k4_trace(int v);
+int read_k4_trace(unsigned long long *host, int n);
 // ADC_OUTLIER_PATH=2 selects the two-launch path (A/B testing).
 bool use_fused_outlier();
 void set_fused_outlier(int v);

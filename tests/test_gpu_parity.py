@@ -320,13 +320,24 @@ def test_graph_replay_matches_eager(torch_cuda, scheme, group):
     assert int(slot.status[0]) == 0
 
 
+K4_PATHS = {"two_launch": 0, "single_pass": 1, "single_pass_spec": 2}
+
+
+def _k4_eligible(shape, group):
+    return group in (32, 64, 128, 256) and shape[1] % group == 0 and shape[1] % 32 == 0 and shape[1] <= 16384
+
+
+@pytest.mark.parametrize("path", sorted(K4_PATHS))
 @pytest.mark.parametrize("shape,dtype_name,group", [
     ((8192, 1024), "bfloat16", 128), ((8192, 4096), "bfloat16", 128), ((8192, 768), "float32", 128),
     ((4096, 4096), "float16", 128), ((333, 1024), "bfloat16", 64), ((1000, 40), "float32", 8),
-    ((64, 4096), "bfloat16", 256), ((16384, 1024), "bfloat16", 128), ((300, 8), "float16", 16)])
-def test_fused_outlier_matches_two_launch_path(torch_cuda, shape, dtype_name, group):
-    """The single-launch cooperative K4 (fused.cu) writes the same bytes as
-    colreduce + quantiser, and both match the oracle; it is one launch."""
+    ((64, 4096), "bfloat16", 256), ((16384, 1024), "bfloat16", 128), ((300, 8), "float16", 16),
+    ((4096, 11008), "bfloat16", 128), ((2048, 8192), "float16", 32),
+    ((7, 512), "bfloat16", 128), ((3, 4096), "float32", 128)])
+def test_outlier_paths_match_oracle(torch_cuda, shape, dtype_name, group, path):
+    """Every outlier-separated compress path writes the oracle's bytes: the
+    two launches (colreduce + quantiser), the single-pass cooperative kernel
+    (k4.cu, one launch where eligible) with and without speculation."""
     torch = torch_cuda
     import paper_2508_00806_b200 as adc
     from paper_2508_00806_b200 import _lib
@@ -337,65 +348,66 @@ def test_fused_outlier_matches_two_launch_path(torch_cuda, shape, dtype_name, gr
     xt = torch.from_numpy(x).to(getattr(torch, dtype_name)).cuda()
     want = oracle_run(xt.cpu().to(torch.float32).numpy(), cases.OUTL, group, 3.0)
     spec = adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED, group)
-    two = device_run(xt, cases.OUTL, group, 3.0)
     try:
-        _lib.set_option("outlier_path", 1)
+        _lib.set_option("outlier_path", K4_PATHS[path])
         n0 = _lib.lib().adc_kernel_launches()
         ct = adc.compress(xt, spec)
         torch.cuda.synchronize()
-        assert _lib.lib().adc_kernel_launches() - n0 == 1
-        fused = device_run(xt, cases.OUTL, group, 3.0)
+        if path != "two_launch" and _k4_eligible(shape, group):
+            assert _lib.lib().adc_kernel_launches() - n0 == 1
+        got = device_run(xt, cases.OUTL, group, 3.0)
     finally:
-        _lib.set_option("outlier_path", 2)
-    assert cases.norm_digest(*fused) == cases.norm_digest(*two) == cases.norm_digest(*want)
+        _lib.set_option("outlier_path", 0)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
     idx = want[0]["idx"]
     assert ct.outlier_count == (0 if idx is None else len(idx))
 
 
-@pytest.mark.parametrize("path", ["fused", "speculative"])
-@pytest.mark.parametrize("dtype_name,cols", [("bfloat16", 1024), ("float32", 768), ("float16", 4096),
-                                             ("bfloat16", 3072)])
-def test_fused_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, path):
-    """A slot's workspace carries the previous call's channel set; the fused
-    kernel (or the speculative first pass of the two-launch path) quantises
-    with it and re-quantises when the actual set differs.  Alternate inputs with different / equal outlier sets
+@pytest.mark.parametrize("path", ["single_pass", "single_pass_spec"])
+@pytest.mark.parametrize("dtype_name,cols,rows", [("bfloat16", 1024, 2048), ("float32", 768, 2048),
+                                                  ("float16", 4096, 2048), ("bfloat16", 3072, 2048),
+                                                  ("bfloat16", 4096, 16384)])
+def test_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, rows, path):
+    """A slot's workspace carries the previous call's channel set (and the
+    double-buffered column accumulator); the speculative single pass
+    quantises with the predicted set and re-quantises the groups whose
+    channels changed.  Alternate inputs with different / equal outlier sets
     through ONE slot and check every call against the oracle."""
     torch = torch_cuda
     import paper_2508_00806_b200 as adc
     from paper_2508_00806_b200.slots import CodecSlot
-    rows = 2048
     rng = np.random.default_rng(cols)
     base = rng.normal(size=(rows, cols)).astype(np.float32)
     sets = [rng.choice(cols, 12, replace=False), rng.choice(cols, 7, replace=False), np.array([], int)]
     seq = [0, 0, 1, 1, 0, 2, 2, 1, 0]
     dt = getattr(torch, dtype_name)
     from paper_2508_00806_b200 import _lib
-    _lib.set_option("outlier_path", 1 if path == "fused" else 2)
-    _lib.set_option("outlier_spec", 1 if path == "speculative" else 0)
-    slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), dt, torch.float32, k_cap=64)
-    y = torch.empty(rows, cols, dtype=torch.float32, device="cuda")
-    for step, si in enumerate(seq):
-        x = base * rng.uniform(0.5, 2.0)
-        x[:, sets[si]] *= 40.0
-        xt = torch.from_numpy(x).to(dt).cuda()
-        sp = torch.cuda.current_stream().cuda_stream
-        slot.compress_ptr(xt.data_ptr(), sp)
-        slot.decompress_ptr(y.data_ptr(), sp)
-        torch.cuda.synchronize()
-        want, wdeq = oracle_run(xt.cpu().to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
-        k = int(slot.k_status[1])
-        got = cases.normalized(slot.scales.cpu().numpy(), None, slot.codes.cpu().numpy(),
-                               slot.idx[:k].cpu().numpy(), slot.val[:k].cpu().numpy(), None)
-        for key in ("scales", "codes", "idx", "vals"):
-            w, g = want[key], got[key]
-            if w is None or w.size == 0:
-                assert g is None or g.size == 0, (step, key)
-            else:
-                np.testing.assert_array_equal(g, w, err_msg=f"step {step} {key}")
-        np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), wdeq.view(np.uint32))
-        assert int(slot.status[0]) == 0
-    _lib.set_option("outlier_path", 2)
-    _lib.set_option("outlier_spec", 0)
+    _lib.set_option("outlier_path", K4_PATHS[path])
+    try:
+        slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), dt, torch.float32, k_cap=64)
+        y = torch.empty(rows, cols, dtype=torch.float32, device="cuda")
+        for step, si in enumerate(seq):
+            x = base * rng.uniform(0.5, 2.0)
+            x[:, sets[si]] *= 40.0
+            xt = torch.from_numpy(x).to(dt).cuda()
+            sp = torch.cuda.current_stream().cuda_stream
+            slot.compress_ptr(xt.data_ptr(), sp)
+            slot.decompress_ptr(y.data_ptr(), sp)
+            torch.cuda.synchronize()
+            want, wdeq = oracle_run(xt.cpu().to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+            k = int(slot.k_status[1])
+            got = cases.normalized(slot.scales.cpu().numpy(), None, slot.codes.cpu().numpy(),
+                                   slot.idx[:k].cpu().numpy(), slot.val[:k].cpu().numpy(), None)
+            for key in ("scales", "codes", "idx", "vals"):
+                w, g = want[key], got[key]
+                if w is None or w.size == 0:
+                    assert g is None or g.size == 0, (step, key)
+                else:
+                    np.testing.assert_array_equal(g, w, err_msg=f"step {step} {key}")
+            np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), wdeq.view(np.uint32))
+            assert int(slot.status[0]) == 0
+    finally:
+        _lib.set_option("outlier_path", 0)
 
 
 @pytest.mark.parametrize("rows", [16384, 16384 + 256])
