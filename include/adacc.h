@@ -77,6 +77,33 @@ extern "C" {
 #define ADC_ERR_TOO_MANY_OUTLIERS 2u
 #define ADC_ERR_K_CAP 4u
 #define ADC_ERR_NONBINARY 8u
+/* adc_deserialize content checks (CorruptPayloadError, codec.py:512-534) */
+#define ADC_ERR_BAD_SCALE 16u       /* a scale is non-finite or negative */
+#define ADC_ERR_BAD_OFFSET 32u      /* an offset is non-finite */
+#define ADC_ERR_BAD_INDEX_RANGE 64u /* an outlier index >= cols */
+#define ADC_ERR_BAD_INDEX_ORDER 128u /* outlier indices not strictly increasing */
+
+/* adc_parse_header verdicts (CorruptPayloadError, codec.py:464-493), in the
+ * reference's check order; ADC_WIRE_OK = the header describes `len` bytes. */
+#define ADC_WIRE_OK 0
+#define ADC_WIRE_TRUNCATED 1      /* len < 25 */
+#define ADC_WIRE_BAD_MAGIC 2
+#define ADC_WIRE_BAD_SCHEME 3
+#define ADC_WIRE_BAD_SHAPE 4      /* rows < 1 or cols < 1 */
+#define ADC_WIRE_OUTLIERS_NOT_ALLOWED 5
+#define ADC_WIRE_TOO_MANY_OUTLIERS 6 /* 2k > cols */
+#define ADC_WIRE_BAD_GROUP_SIZE 7
+#define ADC_WIRE_BAD_GROUP_COUNT 8
+#define ADC_WIRE_SIZE_MISMATCH 9
+
+/* The 25-byte ADC1 header <4sBIIIII> (codec.py:52) and derived sizes. */
+typedef struct {
+  int32_t scheme;
+  uint32_t rows, cols, group_size, group_count, outlier_count;
+  uint64_t expected_groups; /* what the shape implies (ADC_WIRE_BAD_GROUP_COUNT) */
+  uint64_t code_bytes;      /* packed codes, or mask bytes for BIT_MASK */
+  uint64_t total_bytes;     /* 25 + payload (ADC_WIRE_SIZE_MISMATCH) */
+} adc_wire_header;
 
 /* Library / ABI identification. */
 ADC_API const char *adc_version(void);
@@ -187,6 +214,29 @@ ADC_API int adc_serialize(int scheme, const uint16_t *scales, const uint16_t *of
                           const uint16_t *outlier_val, const int32_t *k_dev, int64_t k_cap,
                           int64_t rows, int64_t cols, int64_t group_size, uint8_t *out,
                           size_t out_cap, uint64_t *out_len, uint32_t *err_word, void *stream);
+
+/*
+ * ADC1 header check; the header half of deserialize (codec.py:464-493).
+ * Host-only, no CUDA: reads the first 25 bytes of a HOST copy of the header,
+ * fills *h and returns an ADC_WIRE_* verdict (the first failing check in the
+ * reference's order); `len` is the whole payload's length in bytes.
+ */
+ADC_API int adc_parse_header(const uint8_t *header, uint64_t len, adc_wire_header *h);
+
+/*
+ * Device-side ADC1 deserialisation; the content half of deserialize
+ * (codec.py:494-546).  `in` is the whole payload in DEVICE memory, `h` its
+ * header as accepted by adc_parse_header (ADC_WIRE_OK, else ADC_EINVAL).
+ * Splits the payload into the record's device arrays -- scales (and offsets)
+ * h->group_count uint16 each, codes h->code_bytes (16-byte aligned), outlier
+ * indices k uint32 and values k*rows uint16 -- and ORs ADC_ERR_BAD_* bits into
+ * err_word for non-finite / negative scales, non-finite offsets, indices
+ * >= cols and indices that do not strictly increase.  BIT_MASK: `codes`
+ * receives the mask bytes.
+ */
+ADC_API int adc_deserialize(const uint8_t *in, const adc_wire_header *h, uint16_t *scales,
+                            uint16_t *offsets, uint8_t *codes, uint32_t *outlier_idx,
+                            uint16_t *outlier_val, uint32_t *err_word, void *stream);
 
 /* Column sums of |f16(x)| in float64; replaces channel_abs_sums (codec.py:289-291). */
 ADC_API int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols,

@@ -22,6 +22,18 @@ OK, EINVAL, ECUDA, EWORKSPACE = 0, -1, -2, -3
 _i64, _vp, _sz = C.c_int64, C.c_void_p, C.c_size_t
 _P64 = C.POINTER(C.c_int64)
 
+
+class WireHeader(C.Structure):
+    """adc_wire_header (include/adacc.h)."""
+    _fields_ = [("scheme", C.c_int32), ("rows", C.c_uint32), ("cols", C.c_uint32),
+                ("group_size", C.c_uint32), ("group_count", C.c_uint32), ("outlier_count", C.c_uint32),
+                ("expected_groups", C.c_uint64), ("code_bytes", C.c_uint64), ("total_bytes", C.c_uint64)]
+
+
+(WIRE_OK, WIRE_TRUNCATED, WIRE_BAD_MAGIC, WIRE_BAD_SCHEME, WIRE_BAD_SHAPE, WIRE_OUTLIERS_NOT_ALLOWED,
+ WIRE_TOO_MANY_OUTLIERS, WIRE_BAD_GROUP_SIZE, WIRE_BAD_GROUP_COUNT, WIRE_SIZE_MISMATCH) = range(10)
+ERR_BAD_SCALE, ERR_BAD_OFFSET, ERR_BAD_INDEX_RANGE, ERR_BAD_INDEX_ORDER = 16, 32, 64, 128
+
 SIGNATURES = {
     "adc_version": (C.c_char_p, []),
     "adc_abi_version": (C.c_int, []),
@@ -40,6 +52,8 @@ SIGNATURES = {
     "adc_decompress_int8": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, C.c_int, _vp]),
     "adc_serialize": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
                                 _vp, _vp, _vp]),
+    "adc_parse_header": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(WireHeader)]),
+    "adc_deserialize": (C.c_int, [_vp, C.POINTER(WireHeader), _vp, _vp, _vp, _vp, _vp, _vp, _vp]),
     "adc_channel_abs_sums": (C.c_int, [_vp, C.c_int, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "adc_detect_outliers": (C.c_int, [_vp, C.c_int, _i64, _i64, C.c_double, _i64, _vp, _vp,
                                       _vp, _vp, _sz, _vp]),

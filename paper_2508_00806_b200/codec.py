@@ -192,9 +192,11 @@ def _as_device_matrix(x, *, allow_nd: bool = False) -> torch.Tensor:
         raise ValidationError("activation matrix must have at least one element")
     dev = _device()
     if t.dtype not in _DT:
-        # float64 / integer inputs: one RNE rounding straight to float16, as
-        # np.asarray(x, dtype=float16) does (exact for |int| < 2^53).
-        t = t.to(torch.float64).to(torch.float16)
+        # float64 / integer inputs: numpy's cast, as the reference's
+        # np.asarray(x, dtype=float16) (codec.py:158) -- ONE RNE rounding to
+        # float16.  torch's float64 -> float16 goes through float32 and rounds
+        # twice (1 + 2^-11 + 2^-40 -> 1.0 instead of 1 + 2^-10).
+        t = torch.from_numpy(np.ascontiguousarray(t.detach().cpu().numpy().astype(np.float16)))
     return t.to(dev, non_blocking=True).contiguous()
 
 
@@ -581,72 +583,81 @@ def serialize_device(ct: CompressedTensor) -> torch.Tensor:
     return out[:length]
 
 
-def deserialize(buf: bytes) -> CompressedTensor:
-    """Parse + validate an ADC1 payload onto the device (codec.py:462-546)."""
-    if len(buf) < _HEADER.size:
-        raise CorruptPayloadError(f"payload truncated: {len(buf)} bytes is shorter than the header")
-    magic, scheme_raw, rows, cols, group_size, group_count, k = _HEADER.unpack_from(buf)
-    if magic != MAGIC:
-        raise CorruptPayloadError(f"bad magic {magic!r}")
-    try:
-        scheme = Scheme(scheme_raw)
-    except ValueError:
-        raise CorruptPayloadError(f"unknown scheme byte {scheme_raw}") from None
-    if rows < 1 or cols < 1:
-        raise CorruptPayloadError(f"invalid shape {rows}x{cols}")
-    if scheme is not Scheme.OUTLIER_SEPARATED and k:
-        raise CorruptPayloadError(f"{scheme.name} cannot carry outliers")
-    if 2 * k > cols:
-        raise CorruptPayloadError(f"outlier count {k} exceeds half of {cols} channels")
-    n = rows * cols
-    if scheme is Scheme.BIT_MASK:
-        want_groups = 0
-    elif group_size == PER_CHANNEL:
-        want_groups = cols
-    elif group_size >= 1:
-        want_groups = -(-n // group_size)
+def _header_error(v: int, buf_len: int, raw: bytes, h) -> CorruptPayloadError:
+    """The reference's message for an adc_parse_header verdict (codec.py:464-493)."""
+    if v == _lib.WIRE_TRUNCATED:
+        return CorruptPayloadError(f"payload truncated: {buf_len} bytes is shorter than the header")
+    if v == _lib.WIRE_BAD_MAGIC:
+        return CorruptPayloadError(f"bad magic {bytes(raw[:4])!r}")
+    if v == _lib.WIRE_BAD_SCHEME:
+        return CorruptPayloadError(f"unknown scheme byte {h.scheme}")
+    if v == _lib.WIRE_BAD_SHAPE:
+        return CorruptPayloadError(f"invalid shape {h.rows}x{h.cols}")
+    if v == _lib.WIRE_OUTLIERS_NOT_ALLOWED:
+        return CorruptPayloadError(f"{Scheme(h.scheme).name} cannot carry outliers")
+    if v == _lib.WIRE_TOO_MANY_OUTLIERS:
+        return CorruptPayloadError(f"outlier count {h.outlier_count} exceeds half of {h.cols} channels")
+    if v == _lib.WIRE_BAD_GROUP_COUNT:
+        return CorruptPayloadError(f"group count {h.group_count} does not match shape (want {h.expected_groups})")
+    if v == _lib.WIRE_SIZE_MISMATCH:
+        return CorruptPayloadError(f"payload size mismatch: expected {h.total_bytes} bytes, got {buf_len}")
+    return CorruptPayloadError(f"invalid group size {h.group_size}")
+
+
+_CONTENT_ERRORS = ((_lib.ERR_BAD_SCALE, "scales must be finite and non-negative"),
+                   (_lib.ERR_BAD_OFFSET, "offsets must be finite"),
+                   (_lib.ERR_BAD_INDEX_RANGE, "outlier index out of range"),
+                   (_lib.ERR_BAD_INDEX_ORDER, "outlier indices must be strictly increasing"))
+
+
+def deserialize(buf) -> CompressedTensor:
+    """Parse + validate an ADC1 payload into a device record (codec.py:462-546).
+
+    ``buf`` is ``bytes`` (uploaded once) or a uint8 CUDA tensor already in HBM.
+    The header is checked by ``adc_parse_header`` (host, 25 bytes); the
+    content -- scale / offset finiteness, outlier index range and order -- is
+    checked by the device kernel that splits the payload into the record's
+    arrays (``adc_deserialize``).  Errors are the reference's
+    ``CorruptPayloadError`` messages, raised in the reference's order.
+    """
+    if isinstance(buf, torch.Tensor):
+        if buf.dtype != torch.uint8 or buf.dim() != 1:
+            raise ValidationError("device payload must be a 1-D uint8 tensor")
+        blob_dev, n = buf, buf.numel()
+        head = bytes(buf[:_HEADER.size].cpu().numpy().tobytes()) if n else b""
     else:
-        raise CorruptPayloadError(f"invalid group size {group_size}")
-    if group_count != want_groups:
-        raise CorruptPayloadError(f"group count {group_count} does not match shape (want {want_groups})")
-    expected = _HEADER.size + packed_payload_bytes(scheme, rows, cols, group_size, k)
-    if len(buf) != expected:
-        raise CorruptPayloadError(f"payload size mismatch: expected {expected} bytes, got {len(buf)}")
+        blob = bytes(buf)
+        blob_dev, n, head = None, len(blob), blob[:_HEADER.size]
+    h = _lib.WireHeader()
+    verdict = _lib.lib().adc_parse_header(head, n, _lib.C.byref(h))
+    if verdict != _lib.WIRE_OK:
+        raise _header_error(verdict, n, head, h)
     dev = _device()
-    pos = _HEADER.size
-    if scheme is Scheme.BIT_MASK:
-        bits = torch.from_numpy(np.frombuffer(buf, np.uint8, offset=pos).copy()).to(dev)
-        return CompressedTensor(scheme, rows, cols, 0, None, None, None, mask_bits=bits)
-    if scheme is Scheme.ASYMMETRIC_GROUP:
-        meta = np.frombuffer(buf, "<f2", count=2 * group_count, offset=pos).reshape(-1, 2)
-        scales, offsets = meta[:, 0].copy(), meta[:, 1].copy()
-        pos += 4 * group_count
+    if blob_dev is None:
+        blob_dev = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(dev)
     else:
-        scales = np.frombuffer(buf, "<f2", count=group_count, offset=pos).copy()
-        offsets = None
-        pos += 2 * group_count
-    if not np.isfinite(scales).all() or (scales < 0).any():
-        raise CorruptPayloadError("scales must be finite and non-negative")
-    if offsets is not None and not np.isfinite(offsets).all():
-        raise CorruptPayloadError("offsets must be finite")
-    code_bytes = (n + 1) // 2
-    codes = np.frombuffer(buf, np.uint8, count=code_bytes, offset=pos).copy()
-    pos += code_bytes
-    idx_t = val_t = None
-    if scheme is Scheme.OUTLIER_SEPARATED and k:
-        idx = np.frombuffer(buf, "<u4", count=k, offset=pos).astype(np.int64)
-        pos += 4 * k
-        if (idx >= cols).any():
-            raise CorruptPayloadError("outlier index out of range")
-        if (np.diff(idx) <= 0).any():
-            raise CorruptPayloadError("outlier indices must be strictly increasing")
-        val = np.frombuffer(buf, "<f2", count=k * rows, offset=pos).reshape(k, rows).copy()
-        idx_t = torch.from_numpy(idx).to(dev)
-        val_t = torch.from_numpy(val).to(dev)
-    return CompressedTensor(
-        scheme, rows, cols, group_size, torch.from_numpy(scales).to(dev),
-        None if offsets is None else torch.from_numpy(offsets).to(dev),
-        torch.from_numpy(codes).to(dev), outlier_indices=idx_t, outlier_values=val_t)
+        blob_dev = blob_dev.contiguous()
+    scheme, rows, cols, k = Scheme(h.scheme), int(h.rows), int(h.cols), int(h.outlier_count)
+    gc = int(h.group_count)
+    is_mask = scheme is Scheme.BIT_MASK
+    codes = torch.empty(int(h.code_bytes), dtype=torch.uint8, device=dev)
+    scales = None if is_mask else torch.empty(gc, dtype=torch.float16, device=dev)
+    offsets = torch.empty(gc, dtype=torch.float16, device=dev) if scheme is Scheme.ASYMMETRIC_GROUP else None
+    idx = torch.empty(k, dtype=torch.int32, device=dev) if k else None
+    val = torch.empty((k, rows), dtype=torch.float16, device=dev) if k else None
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    st = _lib.lib().adc_deserialize(blob_dev.data_ptr(), _lib.C.byref(h), _ptr(scales), _ptr(offsets),
+                                    codes.data_ptr(), _ptr(idx), _ptr(val), err.data_ptr(), _stream())
+    _lib.check(st, "deserialize")
+    word = int(err.item()) & 0xffffffff
+    for bit, msg in _CONTENT_ERRORS:
+        if word & bit:
+            raise CorruptPayloadError(msg)
+    if is_mask:
+        return CompressedTensor(scheme, rows, cols, 0, None, None, None, mask_bits=codes)
+    return CompressedTensor(scheme, rows, cols, int(h.group_size), scales, offsets, codes,
+                            outlier_indices=None if idx is None else idx.to(torch.int64),
+                            outlier_values=val)
 
 
 # ---------------------------------------------------------------------------

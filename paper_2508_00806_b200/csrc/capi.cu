@@ -337,6 +337,67 @@ int adc_serialize(int scheme, const uint16_t *scales, const uint16_t *offsets, c
   return check_launch("serialize");
 }
 
+int adc_parse_header(const uint8_t *header, uint64_t len, adc_wire_header *h) {
+  if (!h) return ADC_WIRE_TRUNCATED;
+  std::memset(h, 0, sizeof(*h));
+  if (!header || len < 25) return ADC_WIRE_TRUNCATED;
+  auto u32 = [&](int at) {
+    uint32_t v;
+    std::memcpy(&v, header + at, 4);  // little-endian host (x86-64 / aarch64)
+    return v;
+  };
+  h->scheme = header[4];
+  h->rows = u32(5), h->cols = u32(9), h->group_size = u32(13), h->group_count = u32(17),
+  h->outlier_count = u32(21);
+  if (std::memcmp(header, "ADC1", 4) != 0) return ADC_WIRE_BAD_MAGIC;
+  if (h->scheme > ADC_BIT_MASK) return ADC_WIRE_BAD_SCHEME;
+  if (h->rows < 1 || h->cols < 1) return ADC_WIRE_BAD_SHAPE;
+  const uint64_t k = h->outlier_count, n = static_cast<uint64_t>(h->rows) * h->cols;
+  if (h->scheme != ADC_OUTLIER_SEPARATED && k) return ADC_WIRE_OUTLIERS_NOT_ALLOWED;
+  if (2 * k > h->cols) return ADC_WIRE_TOO_MANY_OUTLIERS;
+  uint64_t meta = 0;
+  if (h->scheme == ADC_BIT_MASK) {
+    h->expected_groups = 0;
+    h->code_bytes = (n + 7) / 8;
+  } else {
+    // u32 group_size is never negative: 0 = PER_CHANNEL (codec.py:482-487)
+    h->expected_groups = h->group_size == ADC_PER_CHANNEL ? h->cols : (n + h->group_size - 1) / h->group_size;
+    h->code_bytes = (n + 1) / 2;
+    meta = h->expected_groups * (h->scheme == ADC_ASYMMETRIC_GROUP ? 4 : 2);
+  }
+  if (h->group_count != h->expected_groups) return ADC_WIRE_BAD_GROUP_COUNT;
+  // n < 2^64 and k * (4 + 2 rows) < 2^63 (k < 2^31, rows < 2^32): no overflow
+  h->total_bytes = 25 + meta + h->code_bytes + k * (4 + 2 * static_cast<uint64_t>(h->rows));
+  if (len != h->total_bytes) return ADC_WIRE_SIZE_MISMATCH;
+  return ADC_WIRE_OK;
+}
+
+int adc_deserialize(const uint8_t *in, const adc_wire_header *h, uint16_t *scales, uint16_t *offsets,
+                    uint8_t *codes, uint32_t *outlier_idx, uint16_t *outlier_val, uint32_t *err_word,
+                    void *stream) {
+  if (!h || !in || !codes || !err_word) return fail(ADC_EINVAL, "null buffer");
+  adc_wire_header chk;
+  uint8_t hdr[25];
+  std::memcpy(hdr, "ADC1", 4);
+  hdr[4] = static_cast<uint8_t>(h->scheme);
+  const uint32_t f[5] = {h->rows, h->cols, h->group_size, h->group_count, h->outlier_count};
+  std::memcpy(hdr + 5, f, sizeof f);
+  if (adc_parse_header(hdr, h->total_bytes, &chk) != ADC_WIRE_OK || chk.total_bytes != h->total_bytes ||
+      chk.code_bytes != h->code_bytes)
+    return fail(ADC_EINVAL, "header not accepted by adc_parse_header");
+  const bool mask = h->scheme == ADC_BIT_MASK;
+  if (!mask && !scales) return fail(ADC_EINVAL, "null scales");
+  if (h->scheme == ADC_ASYMMETRIC_GROUP && !offsets) return fail(ADC_EINVAL, "null offsets");
+  if (h->outlier_count && (!outlier_idx || !outlier_val)) return fail(ADC_EINVAL, "outlier buffers required");
+  if (reinterpret_cast<uintptr_t>(codes) % 16) return fail(ADC_EINVAL, "codes must be 16-byte aligned");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  launch_wire_deserialize(c, in, h->scheme, h->rows, h->cols, mask ? 0 : static_cast<int64_t>(h->group_count),
+                          static_cast<int64_t>(h->code_bytes), h->outlier_count, scales,
+                          h->scheme == ADC_ASYMMETRIC_GROUP ? offsets : nullptr, codes, outlier_idx,
+                          outlier_val, err_word);
+  return check_launch("deserialize");
+}
+
 int adc_channel_abs_sums(const void *x, int in_dtype, int64_t rows, int64_t cols, double *sums,
                          uint32_t *err_word, void *workspace, size_t workspace_bytes,
                          void *stream) {

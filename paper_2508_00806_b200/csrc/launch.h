@@ -156,6 +156,9 @@ int launch_wire_serialize(const Ctx &c, int scheme, int64_t rows, int64_t cols, 
                           const uint8_t *codes, int64_t code_bytes, const uint32_t *idx,
                           const uint16_t *val, const int32_t *k_dev, int64_t k_cap, uint8_t *out,
                           int64_t out_cap, uint64_t *out_len, uint32_t *err);
+int launch_wire_deserialize(const Ctx &c, const uint8_t *in, int scheme, int64_t rows, int64_t cols,
+                            int64_t n_groups, int64_t code_bytes, int64_t k, uint16_t *scales,
+                            uint16_t *offsets, uint8_t *codes, uint32_t *idx, uint16_t *val, uint32_t *err);
 
 // per-channel kernels (channel.cu)
 bool channel_fast_ok(const void *x, int64_t rows, int64_t cols, const void *codes,

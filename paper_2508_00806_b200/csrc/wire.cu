@@ -112,4 +112,101 @@ int launch_wire_serialize(const Ctx &c, int scheme, int64_t rows, int64_t cols, 
   return 0;
 }
 
+// ---------------------------------------------------------------------------
+// Device-side ADC1 deserialisation: the content half of the reference's
+// validator (deserialize, codec.py:506-546) plus the split of the payload
+// into the record's device arrays.  The header half (magic, scheme, shape,
+// counts, total length; codec.py:464-493) is adc_parse_header on the host --
+// it decides the output sizes.  One thread per output unit:
+//   group g          -> scale (and offset) bytes, checked finite / >= 0
+//   16 code bytes    -> one aligned 128-bit store (unaligned byte gathers)
+//   outlier rank j   -> index, checked < cols and > index j-1
+//   8 value halves   -> 16-byte store
+// Violations OR ADC_ERR_BAD_* bits into err (the host raises them in the
+// reference's order: scales, offsets, index range, index order).
+struct UnwireArgs {
+  const uint8_t *in;
+  uint64_t n_groups, code_bytes, k, n_vals;
+  uint64_t m0, c0, i0, v0;  // segment offsets in the payload
+  uint32_t cols;
+  int asym;
+  uint16_t *scales, *offsets;
+  uint8_t *codes;
+  uint32_t *idx;
+  uint16_t *val;
+  uint32_t *err;
+};
+
+__device__ __forceinline__ uint16_t ld_u16(const uint8_t *p) {
+  return static_cast<uint16_t>(p[0] | (static_cast<uint32_t>(p[1]) << 8));
+}
+
+__device__ __forceinline__ uint32_t ld_u32(const uint8_t *p) {
+  return p[0] | (static_cast<uint32_t>(p[1]) << 8) | (static_cast<uint32_t>(p[2]) << 16) |
+         (static_cast<uint32_t>(p[3]) << 24);
+}
+
+__global__ void __launch_bounds__(kThreads) wire_deserialize(UnwireArgs a) {
+  pdl_entry();
+  const uint64_t code_units = (a.code_bytes + 15) / 16, val_units = (a.n_vals + 7) / 8;
+  const uint64_t e0 = a.n_groups, e1 = e0 + code_units, e2 = e1 + a.k, e3 = e2 + val_units;
+  uint32_t bad = 0;
+  for (uint64_t t = static_cast<uint64_t>(blockIdx.x) * kThreads + threadIdx.x; t < e3;
+       t += static_cast<uint64_t>(gridDim.x) * kThreads) {
+    if (t < e0) {
+      const uint8_t *p = a.in + a.m0 + t * (a.asym ? 4 : 2);
+      const uint16_t s = ld_u16(p);
+      // not finite: exponent all ones; negative: sign set on a non-zero value
+      if ((s & 0x7c00u) == 0x7c00u || ((s & 0x8000u) && (s & 0x7fffu))) bad |= ADC_ERR_BAD_SCALE;
+      a.scales[t] = s;
+      if (a.asym) {
+        const uint16_t o = ld_u16(p + 2);
+        if ((o & 0x7c00u) == 0x7c00u) bad |= ADC_ERR_BAD_OFFSET;
+        a.offsets[t] = o;
+      }
+    } else if (t < e1) {
+      const uint64_t q = 16 * (t - e0);
+      const uint8_t *p = a.in + a.c0 + q;
+      if (q + 16 <= a.code_bytes) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) w[j] = ld_u32(p + 4 * j);
+        *reinterpret_cast<uint4 *>(a.codes + q) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {
+        for (uint64_t j = 0; q + j < a.code_bytes; ++j) a.codes[q + j] = p[j];
+      }
+    } else if (t < e2) {
+      const uint64_t j = t - e1;
+      const uint32_t v = ld_u32(a.in + a.i0 + 4 * j);
+      if (v >= a.cols) bad |= ADC_ERR_BAD_INDEX_RANGE;
+      if (j > 0 && v <= ld_u32(a.in + a.i0 + 4 * (j - 1))) bad |= ADC_ERR_BAD_INDEX_ORDER;
+      a.idx[j] = v;
+    } else {
+      const uint64_t q = 8 * (t - e2);
+      const uint8_t *p = a.in + a.v0 + 2 * q;
+      for (uint64_t j = 0; j < 8 && q + j < a.n_vals; ++j) a.val[q + j] = ld_u16(p + 2 * j);
+    }
+  }
+  if (bad) atomicOr(a.err, bad);
+}
+
+int launch_wire_deserialize(const Ctx &c, const uint8_t *in, int scheme, int64_t rows, int64_t cols,
+                            int64_t n_groups, int64_t code_bytes, int64_t k, uint16_t *scales,
+                            uint16_t *offsets, uint8_t *codes, uint32_t *idx, uint16_t *val, uint32_t *err) {
+  const bool asym = scheme == ADC_ASYMMETRIC_GROUP;
+  const uint64_t m0 = 25, c0 = m0 + static_cast<uint64_t>(n_groups) * (asym ? 4 : 2);
+  const uint64_t i0 = c0 + static_cast<uint64_t>(code_bytes), v0 = i0 + 4 * static_cast<uint64_t>(k);
+  UnwireArgs a{in, static_cast<uint64_t>(n_groups), static_cast<uint64_t>(code_bytes), static_cast<uint64_t>(k),
+               static_cast<uint64_t>(k) * static_cast<uint64_t>(rows), m0, c0, i0, v0,
+               static_cast<uint32_t>(cols), asym ? 1 : 0, scales, offsets, codes, idx, val, err};
+  const uint64_t units = a.n_groups + (a.code_bytes + 15) / 16 + a.k + (a.n_vals + 7) / 8;
+  int64_t grid = static_cast<int64_t>((units + kThreads - 1) / kThreads);
+  const int64_t cap = static_cast<int64_t>(c.num_sms) * 8;
+  if (grid > cap) grid = cap;
+  if (grid < 1) grid = 1;
+  launch_k(wire_deserialize, dim3(static_cast<unsigned>(grid)), dim3(kThreads), 0, c.stream, a);
+  note_launches(1);
+  return 0;
+}
+
 }  // namespace adc

@@ -81,3 +81,62 @@ def test_compress_validation_happens_before_any_launch():
     assert lib.adc_compress(2, fake, 0, 4, 8, 128, 3.0, 4, fake, fake, None, fake, fake, fake,
                             fake, None, 0, None) == _lib.EWORKSPACE
     assert "workspace" in _lib.last_error()
+
+
+# ---------------------------------------------------------------- ADC1 header check (host C code)
+_VERDICT_TEXT = {_lib.WIRE_TRUNCATED: "truncated", _lib.WIRE_BAD_MAGIC: "bad magic",
+                 _lib.WIRE_BAD_SCHEME: "unknown scheme", _lib.WIRE_BAD_SHAPE: "invalid shape",
+                 _lib.WIRE_OUTLIERS_NOT_ALLOWED: "cannot carry outliers",
+                 _lib.WIRE_TOO_MANY_OUTLIERS: "exceeds half", _lib.WIRE_BAD_GROUP_COUNT: "group count",
+                 _lib.WIRE_SIZE_MISMATCH: "size mismatch"}
+
+
+def _blobs():
+    import numpy as np
+    rng = np.random.default_rng(11)
+    x = rng.normal(size=(6, 256)).astype(np.float32)
+    x[:, 5] *= 80
+    out = []
+    for scheme, group in ((0, 128), (0, 0), (0, 7), (1, 32), (2, 128), (3, 0)):
+        data = (x > 0).astype(np.uint8) if scheme == 3 else x
+        out.append(orc.serialize(orc.compress(data, scheme, group)))
+    return out
+
+
+def _header_verdict(blob):
+    h = _lib.WireHeader()
+    return _lib.lib().adc_parse_header(blob[:25], len(blob), C.byref(h)), h
+
+
+def test_parse_header_accepts_every_scheme():
+    for blob in _blobs():
+        v, h = _header_verdict(blob)
+        assert v == _lib.WIRE_OK
+        assert h.total_bytes == len(blob)
+
+
+def test_parse_header_matches_reference_validator(reference_codec):
+    """Every single-byte corruption of every header byte (and truncations /
+    extensions) gets the reference deserialize's verdict (codec.py:464-493)."""
+    checked = 0
+    for blob in _blobs():
+        variants = [blob[:n] for n in (0, 10, 24, 25, len(blob) - 1)] + [blob + b"\0"]
+        for at in range(25):
+            for flip in (0x01, 0x80, 0xFF):
+                b = bytearray(blob)
+                b[at] ^= flip
+                variants.append(bytes(b))
+        for b in variants:
+            v, _ = _header_verdict(b)
+            try:
+                reference_codec.deserialize(b)
+                ref = None
+            except reference_codec.CorruptPayloadError as e:
+                ref = str(e)
+            if v == _lib.WIRE_OK:
+                # header accepted: the reference either accepts or rejects on CONTENT
+                assert ref is None or not any(t in ref for t in _VERDICT_TEXT.values()), (b[:25], ref)
+            else:
+                assert ref is not None and _VERDICT_TEXT[v] in ref, (v, ref)
+            checked += 1
+    assert checked > 400
