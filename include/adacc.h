@@ -115,29 +115,26 @@ ADC_API unsigned long long adc_kernel_launches(void);
 
 /*
  * Kernel-path selection (tuning / A-B testing; results are identical):
- *   "compress_path" 1 = TMA-fed streaming group compress, 0 = register path (default).
- *   "outlier_spec"  1 = speculative first pass of the two-launch outlier path
- *                   (column sums + quantisation with the previous call's
- *                   channel set in one read; 0 default).  ADC_OUTLIER_SPEC=1.
  *   "pdl"           1 = launch with programmatic dependent launch (0 default).
  *   "epl"           32 (default) or 16 elements per lane in the group
  *                   quantisers (also ADC_EPL=16).
- *   "outlier_path"  1 = single-launch cooperative outlier-separated compress
- *                   (where eligible), 2 = column-statistics launch + quantiser
- *                   launch (default: measured faster).  Also ADC_OUTLIER_PATH=1.
- * Also settable once per process by ADC_COMPRESS_PATH=tma.
+ *   "outlier_path"  0 = column-statistics launch + quantiser launch, 1 = the
+ *                   single-pass cooperative kernel wherever eligible, 2 =
+ *                   automatic (default: the single pass for tall tensors of
+ *                   <= 1024 columns, >= 2^25 elements, where it measured
+ *                   faster).  Also ADC_OUTLIER_PATH=0/1/2.
+ *   "k4_trace"      1 = record the single-pass kernel's phase timestamps.
+ *   "k4_dbg"        timing experiments only (1 = stop the single pass after
+ *                   its streaming phase; results invalid).
  */
 ADC_API int adc_set_option(const char *key, int value);
 
 /*
- * Tuning aid: with adc_set_option("trace", 1), the single-launch
+ * Tuning aid: with adc_set_option("k4_trace", 1) the single-pass
  * outlier-separated kernel records per-CTA phase timestamps; this copies the
- * last launch's records (8 u64 per CTA: globaltimer at entry, then clock64
- * deltas at the end of each phase) to host memory.  Returns the count copied.
+ * last launch's records (64 u64 per CTA: globaltimer at entry, clock64 deltas
+ * at phase ends, per-warp entry / exit) to host memory.  Returns the count.
  */
-ADC_API int adc_debug_trace(unsigned long long *out, int n);
-/* Same for the single-pass outlier-separated kernel (adc_set_option("k4_trace", 1)):
- * 16 u64 per CTA (globaltimer at entry, clock64 deltas at phase ends). */
 ADC_API int adc_debug_trace_k4(unsigned long long *out, int n);
 
 /*

@@ -40,7 +40,6 @@ SIGNATURES = {
     "adc_last_error": (C.c_char_p, []),
     "adc_kernel_launches": (C.c_ulonglong, []),
     "adc_set_option": (C.c_int, [C.c_char_p, C.c_int]),
-    "adc_debug_trace": (C.c_int, [_vp, C.c_int]),
     "adc_debug_trace_k4": (C.c_int, [_vp, C.c_int]),
     "adc_payload_bytes": (C.c_int, [C.c_int, _i64, _i64, _i64, _i64, _P64, _P64, _P64]),
     "adc_workspace_bytes": (_sz, [C.c_int, _i64, _i64, _i64]),

@@ -21,7 +21,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 OUT_DIR = PKG / "_lib"
 LIB = OUT_DIR / "libadacc.so"
-SOURCES = ["k4.cu", "group.cu", "stream.cu", "channel.cu", "outlier.cu", "fused.cu", "int8.cu", "wire.cu", "mask.cu", "capi.cu"]
+SOURCES = ["k4.cu", "group.cu", "channel.cu", "outlier.cu", "int8.cu", "wire.cu", "mask.cu", "capi.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-fvisibility=hidden", "--expt-relaxed-constexpr",

@@ -108,14 +108,6 @@ unsigned long long adc_kernel_launches(void) { return g_launches.load(std::memor
 int adc_set_option(const char *key, int value) {
   if (!key) return fail(ADC_EINVAL, "null option key");
   const std::string k(key);
-  if (k == "compress_path") {  // 1: TMA-fed streaming kernel, 0: register path (default)
-    set_compress_path(value);
-    return ADC_OK;
-  }
-  if (k == "outlier_spec") {  // speculative single-read first pass (1) / plain two launches (0, default)
-    set_outlier_spec(value);
-    return ADC_OK;
-  }
   if (k == "pdl") {  // programmatic dependent launch on (1) / off (0, default)
     set_pdl(value);
     return ADC_OK;
@@ -124,12 +116,12 @@ int adc_set_option(const char *key, int value) {
     set_epl(value);
     return ADC_OK;
   }
-  if (k == "trace") {  // record phase timestamps of the fused kernel (adc_debug_trace)
-    set_fused_trace(value);
+  if (k == "outlier_path") {  // 0: colreduce + quantiser, 1: single pass where eligible, 2: automatic (default)
+    set_k4_mode(value);
     return ADC_OK;
   }
-  if (k == "outlier_path") {  // 0: colreduce + quantiser, 1: single pass (default), 2: single pass + speculation
-    set_k4_mode(value);
+  if (k == "k4_dbg") {  // timing experiments on the single-pass kernel (results invalid when != 0)
+    set_k4_dbg(value);
     return ADC_OK;
   }
   if (k == "k4_trace") {  // record phase timestamps of the single-pass kernel (adc_debug_trace_k4)
@@ -139,11 +131,6 @@ int adc_set_option(const char *key, int value) {
   return fail(ADC_EINVAL, "unknown option");
 }
 
-int adc_debug_trace(unsigned long long *out, int n) {
-  if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
-  const int r = read_fused_trace(out, n);
-  return r < 0 ? fail(ADC_ECUDA, "trace copy failed") : r;
-}
 
 int adc_debug_trace_k4(unsigned long long *out, int n) {
   if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
@@ -215,17 +202,6 @@ int adc_compress(int scheme, const void *x, int in_dtype, int64_t rows, int64_t 
     if (launch_outlier_k4(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws, codes, scales,
                           outlier_idx, outlier_val, k_out, err_word))
       return check_launch("outlier_single_pass");
-    if (launch_outlier_fused(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
-                             codes, scales, outlier_idx, outlier_val, k_out, err_word))
-      return check_launch("outlier_fused");
-    if (k_cap > 0 && launch_outlier_spec(c, x, in_dtype, rows, cols, group_size, z_threshold, k_cap, ws,
-                                         codes, scales, outlier_idx, k_out, err_word, ws.counters + 3)) {
-      rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag, outlier_idx,
-                                  k_out, outlier_val, k_cap, codes, scales, nullptr, err_word,
-                                  ws.counters + 3);
-      if (rc) return fail(ADC_EINVAL, "outlier dispatch");
-      return check_launch("outlier_speculative");
-    }
     rc |= launch_colstats_sum(c, x, in_dtype, rows, cols, ws, true, z_threshold, k_cap,
                               outlier_idx, k_out, err_word, true);
     rc |= launch_group_compress(c, x, in_dtype, rows, cols, group_size, false, ws.flag,
@@ -270,12 +246,6 @@ int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
   if (asym && !offsets) return fail(ADC_EINVAL, "null offsets");
   const bool pc = group_size == ADC_PER_CHANNEL;
   int rc = 0;
-  if (scheme == ADC_OUTLIER_SEPARATED && k_cap > 0 && outlier_idx && outlier_val && k_dev && !pc) {
-    rc = launch_outlier_decompress(c, codes, scales, outlier_idx, outlier_val, k_dev, k_cap, rows, cols,
-                                   group_size, y, out_dtype);
-    if (rc < 0) return fail(ADC_EINVAL, "decompress dispatch");
-    if (rc == 0) return check_launch("outlier_decompress");
-  }
   if (pc && !asym && channel_fast_ok(y, rows, cols, codes, scales) &&
       reinterpret_cast<uintptr_t>(y) % 16 == 0) {
     rc = launch_channel_decompress(c, codes, scales, rows, cols, y, out_dtype);

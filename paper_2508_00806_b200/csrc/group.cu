@@ -407,78 +407,6 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// Outlier-separated decompress in ONE launch (dequantize + the overwrite of
-// the flagged channels, codec.py:278-285): the plain grid-stride symmetric
-// dequantiser plus a per-CTA column -> rank map in shared memory (built from
-// the ascending index list).  A unit whose 8 columns hold a flagged channel
-// (k/cols of them) issues the load of its stored float16 value(s) BEFORE the
-// dequantisation of the iteration and writes the 2-byte override(s) after the
-// unit's 16-byte store (same thread, same address: program order), so the
-// side-buffer latency hides behind the iteration's other work.
-template <int OT, int L, int U>
-__global__ void __launch_bounds__(kThreads)
-    group_dequant_outl8(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
-                        int64_t n_units, FastDiv dcu, int64_t rows, const uint32_t *__restrict__ idx,
-                        const uint16_t *__restrict__ val, const int32_t *__restrict__ k_dev,
-                        int64_t k_cap, void *__restrict__ y) {
-  pdl_entry();
-  extern __shared__ __align__(16) int16_t rank_of[];  // [cols], -1 = kept channel
-  const int cols = static_cast<int>(dcu.d) * 8;
-  const int k = static_cast<int>(min(static_cast<int64_t>(*k_dev), k_cap));
-  for (int c = threadIdx.x; c < cols; c += kThreads) rank_of[c] = -1;
-  __syncthreads();
-  for (int i = threadIdx.x; i < k; i += kThreads) rank_of[__ldg(idx + i)] = static_cast<int16_t>(i);
-  __syncthreads();
-  const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * U;
-  for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * U; base < n_units; base += step) {
-    uint32_t w[U], fm[U], row[U], ucol[U];
-    float hv[U];
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int64_t u = base + q * kThreads + threadIdx.x;
-      w[q] = (u < n_units) ? __ldcs(codes + u) : 0u;
-      row[q] = fastdiv(static_cast<uint32_t>(u), dcu);
-      ucol[q] = static_cast<uint32_t>(u) - row[q] * dcu.d;
-      fm[q] = 0;
-      hv[q] = 0.f;
-      if (u < n_units) {
-        const uint4 rk = *reinterpret_cast<const uint4 *>(rank_of + 8 * ucol[q]);
-        if ((rk.x & rk.y & rk.z & rk.w) != 0xffffffffu) {  // a flagged channel (rare)
-          const uint32_t ws[4] = {rk.x, rk.y, rk.z, rk.w};
-#pragma unroll
-          for (int j = 0; j < 8; ++j) fm[q] |= ((ws[j >> 1] >> (16 * (j & 1))) & 0x8000u) ? 0u : (1u << j);
-          const int j0 = __ffs(fm[q]) - 1;
-          const int r0 = static_cast<int16_t>(rank_of[8 * ucol[q] + j0]);
-          hv[q] = h2f(__ldg(val + static_cast<int64_t>(r0) * rows + row[q]));  // in flight
-        }
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      const int64_t u = base + q * kThreads + threadIdx.x;
-      if (u >= n_units) continue;
-      const float sc = h2f(__ldg(scales + u / L));
-      float v[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) v[j] = deq<false>(nib_code(w[q], j), sc, 0.f);
-      Storer<OT>::store8(y, u * 8, v);
-    }
-#pragma unroll
-    for (int q = 0; q < U; ++q) {
-      if (!fm[q]) continue;
-      const int64_t e = (base + q * kThreads + threadIdx.x) * 8;
-      uint32_t m = fm[q];
-      const int j0 = __ffs(m) - 1;
-      Storer<OT>::store1(y, e + j0, hv[q]);
-      for (m &= m - 1; m; m &= m - 1) {  // more than one flagged channel in 8 columns
-        const int j = __ffs(m) - 1;
-        const int r = static_cast<int16_t>(rank_of[8 * ucol[q] + j]);
-        Storer<OT>::store1(y, e + j, h2f(__ldg(val + static_cast<int64_t>(r) * rows + row[q])));
-      }
-    }
-  }
-}
-
 // ---------------------------------------------------------------------------
 // generic fallbacks: any group size (incl. PER_CHANNEL), any shape/alignment
 // ---------------------------------------------------------------------------
@@ -655,20 +583,6 @@ __global__ void __launch_bounds__(kThreads)
 // ---------------------------------------------------------------------------
 // host launchers
 // ---------------------------------------------------------------------------
-static std::atomic<int> g_compress_path{-1};
-
-bool use_tma_compress() {
-  int v = g_compress_path.load(std::memory_order_relaxed);
-  if (v < 0) {
-    const char *e = getenv("ADC_COMPRESS_PATH");
-    v = (e && e[0] == 't') ? 1 : 0;  // measured: the register path is faster for now
-    g_compress_path.store(v, std::memory_order_relaxed);
-  }
-  return v == 1;
-}
-
-void set_compress_path(int v) { g_compress_path.store(v ? 1 : 0, std::memory_order_relaxed); }
-
 // 32 elements per lane (one 128-bit code store, the group's scale work
 // amortised over twice the elements) vs 16; ADC_EPL=16 or
 // adc_set_option("epl", 16) selects the 16-element kernels (A/B testing).
@@ -681,13 +595,6 @@ bool use_epl32() {
     g_epl.store(v, std::memory_order_relaxed);
   }
   return v == 32;
-}
-// One-launch outlier decompress: measured 3588 vs 3626 GB/s on the bench
-// step (its dequantiser runs 2 units in flight and pays the rank map; the
-// scatter it saves is short), so it is opt-in: ADC_OUTLIER_DEQ1=1.
-bool use_one_launch_outlier_decompress() {
-  const char *e = getenv("ADC_OUTLIER_DEQ1");
-  return e && e[0] == '1';
 }
 void set_epl(int v) { g_epl.store(v == 16 ? 16 : 32, std::memory_order_relaxed); }
 
@@ -768,15 +675,7 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
   const FastDiv dc = make_fastdiv(static_cast<uint32_t>(cols >= 8 ? cols / 8 : 1));  // zero_flags8
   OutlierSide side = outlier_side(c, idx, k_dev, zero ? k_cap : 0, rows, cols, outl_val);
   side.requant = zero ? requant : nullptr;
-  int L = pc ? 0 : lanes_for_group(g, 8);
-  if (L > 0 && use_tma_compress() && n % 8 == 0 && aligned(x, 16) && aligned(codes, 4) && zero_ok &&
-      (!zero || n < (1ll << 31))) {
-    const int rc = launch_group_compress_tma(c, x, dt, rows, cols, L, asym, zero_flag, codes,
-                                             scales, offsets, err);
-    if (rc || !zero) return rc;
-    return launch_outlier_gather(c, x, dt, idx, k_dev, k_cap, rows, cols, outl_val);
-  }
-  L = pc ? 0 : lanes_for_group(g, 32);
+  int L = pc ? 0 : lanes_for_group(g, 32);
   if (L > 0 && use_epl32() && n % 32 == 0 && aligned(x, 16) && aligned(codes, 16) && zero_ok) {
     const int64_t n_units = n / 32;
     const int64_t n_units_pad = (n_units + L - 1) / L * L;
@@ -937,27 +836,6 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
       launch_k(group_dequant_generic<OT, false>, grid, kThreads, 0, c.stream, codes, scales, nullptr,
                                                                         n, g, pc, rows, cols, y), note_launches(1);
   });
-  return 0;
-}
-
-int launch_outlier_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
-                              const uint32_t *idx, const uint16_t *val, const int32_t *k_dev,
-                              int64_t k_cap, int64_t rows, int64_t cols, int64_t g, void *y, int ot) {
-  const int64_t n = rows * cols;
-  const int L = lanes_for_group(g, 8);
-  if (!use_one_launch_outlier_decompress() || L <= 0 || cols % 8 || cols > 16384 || n >= (1ll << 31) ||
-      n * (ot == ADC_F32 ? 4 : 2) > (128ll << 20) || !aligned(y, 16) || !aligned(codes, 4))
-    return 1;  // dequantise + scatter / sector patch
-  const int64_t n_units = n / 8;
-  const int grid = grid_for(c, n_units, kThreads * kUnroll);
-  const FastDiv dcu = make_fastdiv(static_cast<uint32_t>(cols / 8));
-  const size_t smem = static_cast<size_t>(cols) * 2;
-  const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
-  ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {
-    launch_k(group_dequant_outl8<OT, LL, kUnroll>, grid, kThreads, smem, c.stream, codes32, scales, n_units,
-             dcu, rows, idx, val, k_dev, k_cap, y);
-    note_launches(1);
-  }));
   return 0;
 }
 

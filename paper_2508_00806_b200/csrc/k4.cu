@@ -2,55 +2,49 @@
 // persistent cooperative kernel, one 512-thread CTA per SM, the input read
 // from HBM once.
 //
-//   A. Each CTA owns a contiguous slab of rows, cut into chunks of whole rows
-//      that the TMA engine copies into shared memory (cp.async.bulk, one
-//      mbarrier per slot).  The leading chunks stay resident; when the slab
-//      is larger than shared memory the rest streams through a ring of slots
-//      (the last warp done with a ring chunk issues the copy that refills its
-//      slot).  Every chunk is read twice from shared memory:
-//        - column sums: thread (p, uc) owns the 8-column unit uc of rows
-//          p, p + P, ..., so its float64 |x| partial sums stay in registers.
-//          |h| becomes the float64 bit pattern with two integer ops (an f16
-//          value is an exact float32; its bits >> 3 plus the exponent re-bias
-//          are the float64 high word) and one DADD -- no conversion unit;
-//        - with SPEC, quantisation right away with the previous call's
-//          channel set (kept in the workspace): a lane owns 32 consecutive
-//          columns of a row (a group of 128 is 4 lanes).
-//   B. The P row lanes are folded in shared memory; the CTA's column partials
-//      go into a global accumulator with ONE bulk reduction (cp.reduce.async
-//      .bulk .add.f64 = UBLKRED: the adds happen in L2, no per-column
-//      atomics).  Grid barrier: one release-add per CTA on a monotonic
-//      counter, acquire polls against a base kept in the workspace (no
-//      returning same-address atomics -- those serialise at ~150 x 27 cycles).
-//   C. Every CTA reads the sums and evaluates mean / std / z / flags / ranks
-//      itself (numpy's pairwise tree, host-built), so no CTA waits on a
-//      single finisher.  The accumulator is double-buffered: each call zeroes
-//      the buffer the next call uses.  CTA 0 publishes k, the indices and the
-//      new prediction.
-//   D. Quantisation with the actual channel set (codec.py:328-330), from
-//      shared memory for resident chunks and from L2 for streamed ones; with
-//      SPEC only the 128-groups holding a channel whose flag changed.
-//   E. The float16 values of the flagged channels of the slab's rows go to
-//      the (k, rows) side buffer (codec.py:339-340), coalesced along rows.
+// Tiling.  The grid is strips x slabs: a CTA owns the rows [r0, r1) of one
+// column strip of at most 1024 columns (whole 128-groups).  Its tile reaches
+// shared memory through the TMA engine in 16 KB chunks of whole tile rows
+// (cp.async.bulk, one mbarrier per slot).  If the tile fits, every chunk stays
+// resident; otherwise the chunks stream through a ring of slots.
 //
-// Exactness: every f16 value is an integer multiple
-// of 2^-24 below 2^16, so every float64 partial sum -- thread, fold, bulk
-// reduction -- is exact, hence independent of order, while a column total is
-// below 2^29.  Zero elements contribute 2^-127 (the re-biased pattern of 0),
-// which vanishes exactly against any non-zero partial (< half an ulp of
-// 2^-24) and is snapped back to 0 for all-zero columns.  A total that reaches
-// 2^29 (rounding is monotone, so it is seen whatever the order) makes every
-// CTA recompute its share of the columns in numpy's row order (slow, exact),
-// behind a second barrier.  An f16 inf / NaN enters a sum as >= 2^128
-// (finite f16 sums stay below 2^47): NonFiniteInputError.  bf16 inputs:
-// |x| in [2^-17, 65536) is exactly representable in f16, so the bf16 value
-// IS f16(x); a unit holding a zero or a value outside that range converts
-// each element (numpy's astype(float16) of the value).
+// Thread (p, u) owns the 16 columns [16u, 16u + 16) of the strip in the rows
+// p, p + P, ... (P = 512 / (W / 16) row lanes).  A 128-group is 8 lanes.  For
+// every row it holds, from two conflict-free 16-byte shared loads:
+//   A1. column |x| sums: |h| as f32 (shared with the quotients below) ->
+//       float64 (F2F) -> one DADD into 16 per-thread accumulators;
+//   A2. the group's symmetric codes with the PREDICTED channel set zeroed
+//       (the previous call's flags, kept in the workspace; zero-filled = "no
+//       outliers"): group abs-max over 8 lanes, scale, Markstein-rounded
+//       quotients two per FFMA2, saturating nibble pack, 8-byte code store.
+// B.  The P row lanes are folded through shared memory and the strip's column
+//     partials go to a global float64 accumulator with ONE bulk reduction
+//     (cp.reduce.async.bulk .add.f64, in L2); grid barrier = one release-add
+//     per CTA on a monotonic counter + acquire polls.
+// C.  Every CTA reads the column totals and evaluates mean / std / z / flags /
+//     ranks itself (numpy's pairwise tree, host-built), no finisher CTA.
+// D.  Groups whose channel set differs from the prediction are re-quantised
+//     (from shared memory when resident, else from global memory).  When the
+//     prediction holds -- steady state: outlier channels persist (PAPER.md
+//     Fig. 4a) -- D does nothing and x was read exactly once.
+// E.  The float16 values of the flagged channels go to the (k, rows) side
+//     buffer (codec.py:339-340).
 //
-// Eligibility (host side): g in {32, 64, 128, 256}, cols % g == 0,
-// cols % 32 == 0, cols <= 16384, aligned buffers, n < 2^31.  Otherwise the
-// caller uses the two-launch path (colreduce + group_quant_fast), which
-// produces identical bytes.
+// Exactness: f16 values are integer multiples of
+// 2^-24 below 2^16, so every float64 partial sum -- thread, fold, bulk
+// reduction -- is exact (hence order-free) while a column total is below
+// 2^29.  A finite total >= 2^29
+// makes every CTA recompute its share of the columns in numpy's row order
+// (slow, exact) behind a second barrier.  Non-finite elements (f16 overflow,
+// inf, NaN) are caught by the group abs-max (A2/D), by the side-buffer
+// gather (A/E) and by non-finite column totals.  bf16: |x| in [2^-17, 65536)
+// is exactly representable in f16, so such values ARE f16(x); a 16-element
+// unit holding a smaller value converts each element (numpy's
+// astype(float16)).
+//
+// Eligibility (host side): g = 128, cols % 128 == 0, cols <= 16384, bf16 or
+// f16 input, 16-byte aligned buffers, n < 2^31.  Otherwise the caller uses
+// the two-launch path (colreduce + group_quant_fast), identical bytes.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -65,25 +59,25 @@
 
 namespace adc {
 
-constexpr int kK4T = 512;            // threads per CTA
-constexpr int kK4Warps = kK4T / 32;
-constexpr int kK4MaxLeaves = 128;    // cols <= 16384
-constexpr int kK4MaxSlots = 24;
-constexpr double kK4Exact = 536870912.0;     // 2^29
-constexpr uint32_t kF64Rebias = 896u << 20;  // (1023 - 127) << 20
+constexpr int kOT = 512;  // threads per CTA
+constexpr int kOW = kOT / 32;
+constexpr int kOMaxSlots = 16;
+constexpr int kOMaxLeaves = 128;  // cols <= 16384
+constexpr int kOStripCols = 1024;
+constexpr double kOExact = 536870912.0;  // 2^29
 
 // numpy's pairwise_sum_DOUBLE tree for n = cols (block 128, unroll 8, split
 // n/2 - (n/2) % 8), flattened on the host: leaves left to right, internal
 // nodes ordered by height (node ids: leaves 0..nl-1, internal nl + j).
-struct K4Tree {
+struct OTree {
   int n_leaves, n_levels;
-  int16_t leaf_lo[kK4MaxLeaves];
-  uint8_t leaf_n[kK4MaxLeaves];  // 1..128
-  uint8_t left[kK4MaxLeaves], right[kK4MaxLeaves];
+  int16_t leaf_lo[kOMaxLeaves];
+  uint8_t leaf_n[kOMaxLeaves];  // 1..128
+  uint8_t left[kOMaxLeaves], right[kOMaxLeaves];
   uint8_t level_end[16];  // internal nodes of height <= h + 1: [0, level_end[h])
 };
 
-static bool build_k4_tree(int n, K4Tree &t) {
+static bool build_tree(int n, OTree &t) {
   struct Internal { int l, r, h; };
   std::vector<Internal> in;
   std::vector<std::pair<int, int>> leaves;
@@ -99,13 +93,13 @@ static bool build_k4_tree(int n, K4Tree &t) {
   };
   rec(0, n);
   const int nl = static_cast<int>(leaves.size()), ni = static_cast<int>(in.size());
-  if (nl > kK4MaxLeaves || nl + ni > 255) return false;
+  if (nl > kOMaxLeaves || nl + ni > 255) return false;
   std::vector<int> order(ni), pos(ni);
   for (int i = 0; i < ni; ++i) order[i] = i;
   std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return in[x].h < in[y].h; });
   for (int i = 0; i < ni; ++i) pos[order[i]] = i;
   auto id = [&](int enc) { return enc >= 0 ? enc : nl + pos[-enc - 1]; };
-  t = K4Tree{};
+  t = OTree{};
   t.n_leaves = nl;
   for (int i = 0; i < nl; ++i) {
     t.leaf_lo[i] = static_cast<int16_t>(leaves[i].first);
@@ -123,455 +117,654 @@ static bool build_k4_tree(int n, K4Tree &t) {
   return levels <= 16;
 }
 
-struct K4Args {
-  const void *x;
+struct OArgs {
+  const uint16_t *x;
   int64_t rows, cols;
-  int ucols;        // cols / 8: 8-column units per row
-  int P;            // sum mapping: row lanes (J == 1) -- thread (p, uc)
-  int Q, P2;        // quantise mapping: 32-column quads per row, row lanes
-  int chunk_rows;   // rows per chunk (one bulk copy)
-  int n_res;        // chunks kept resident (slots 0 .. n_res-1)
-  int n_ring;       // ring slots behind them (0: the slab is fully resident)
-  int slot_bytes;   // chunk_rows * row bytes, 128-aligned
-  int keep;         // ring chunks stay in L2 (evict_last) for phase D
+  int strips, slabs;  // grid = strips * slabs
+  int rbase, rrem;    // slab i holds rbase + (i < rrem) rows
+  int chunk_rows;     // rows per chunk (one chunk = chunk_rows * strip width * 2 bytes <= slot_bytes)
+  int n_slots;        // shared slots; a CTA whose chunks all fit keeps them resident
+  int slot_bytes;
+  int stats_off;      // byte offset of the statistics area (0: overlays the slots, streamed tiles)
+  int pred_off;       // byte offset of the predicted flags (cols + 16 bytes, never overlaid)
   double thr;
   int64_t k_cap;
-  double *sacc;     // [2][cols] float64 column accumulators (double-buffered, zero at rest)
+  double *sacc;     // [2][cols] scaled float64 column accumulators (double-buffered, zero at rest)
   double *sseq;     // [cols] numpy row-order sums (only when some total >= 2^29)
   uint32_t *ctl;    // [0] barrier arrivals (monotonic), [1] their base for the next call,
                     // [2] epoch (accumulator parity), [3] cols of the last call
-  uint8_t *pflag;   // [cols + 8] previous call's flags (the SPEC prediction)
-  uint32_t *codes;
+  uint8_t *pflag;   // [cols] previous call's flags (the prediction)
+  uint8_t *codes;
   uint16_t *scales;
   uint32_t *idx;
   uint16_t *val;
   int32_t *k_out;
   uint32_t *err;
   int trace;
-  K4Tree tree;
+  int dbg;        // timing experiments only (adc_set_option("k4_dbg")): 1 exit after A (results invalid)
+  OTree tree;
 };
 
 // Phase timestamps of the last traced launch (tuning): per CTA, [0]
 // globaltimer at entry, then clock64 deltas at phase ends.
-constexpr int kK4TraceSlots = 64;  // [0..15] CTA phases (thread 0), [32+w] / [48+w] warp w entry / exit
-constexpr int kK4TraceCtas = 1024;
-__device__ unsigned long long g_k4trace[kK4TraceCtas * kK4TraceSlots];
+constexpr int kOTraceSlots = 64;  // [0..15] CTA phases (thread 0), [32+w] / [48+w] warp w entry / exit
+constexpr int kOTraceCtas = 1024;
+__device__ unsigned long long g_k4trace[kOTraceCtas * kOTraceSlots];
 #define K4TRACE(slot)                                                                            \
   do {                                                                                           \
-    if (a.trace && tid == 0 && b < kK4TraceCtas)                                                 \
-      g_k4trace[b * kK4TraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - t_0); \
+    if (a.trace && tid == 0 && b < kOTraceCtas)                                                  \
+      g_k4trace[b * kOTraceSlots + (slot)] = static_cast<unsigned long long>(clock64() - t_0); \
   } while (0)
 
-__device__ __forceinline__ uint32_t k4_ld_acquire(const uint32_t *p) {
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void grid_arrive(uint32_t *cnt) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+}
+__device__ __forceinline__ void grid_wait(const uint32_t *cnt, uint32_t target) {
+  while (static_cast<int32_t>(ld_acquire_u32(cnt) - target) < 0) {
+  }
+}
+// thread 0 arrives and waits; the CTA synchronises around it
+__device__ __forceinline__ void cta_grid_sync(uint32_t *cnt, uint32_t target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    grid_arrive(cnt);
+    grid_wait(cnt, target);
+  }
+  __syncthreads();
+}
 
-__device__ __forceinline__ double k4_f64_hi(uint32_t hi) { return __hiloint2double(static_cast<int>(hi), 0); }
-
-// |h| of the 8 elements of a unit added to acc[0..7] (column order).
-// f16 words: h -> f32 (exact) -> float64 pattern.  bf16 words (BF): the
-// float32 pattern of a bf16 value is its bits << 16.
+// Rare quantiser cases (kept out of line: the hot loop must stay small for
+// the instruction cache): a subnormal or zero scale, or a bf16 group whose
+// maximum is so small that the f16 rounding of its elements matters.
 template <bool BF>
-__device__ __forceinline__ void k4_colsum8(double *acc, const uint32_t *w) {
-  if (BF) {
-    uint32_t m = __vminu2(w[0] & 0x7fff7fffu, w[1] & 0x7fff7fffu);
-    uint32_t M = __vmaxu2(w[0] & 0x7fff7fffu, w[1] & 0x7fff7fffu);
-    m = __vminu2(m, __vminu2(w[2] & 0x7fff7fffu, w[3] & 0x7fff7fffu));
-    M = __vmaxu2(M, __vmaxu2(w[2] & 0x7fff7fffu, w[3] & 0x7fff7fffu));
-    if (min(m & 0xffffu, m >> 16) >= 0x3700u && max(M & 0xffffu, M >> 16) < 0x4780u) {
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        // low half: ((w & 0x7fff) << 13) + rebias; high half: ((w & 0x7fff0000) >> 3) + rebias
-        acc[2 * i] = __dadd_rn(acc[2 * i], k4_f64_hi((w[i] & 0x7fffu) * 8192u + kF64Rebias));
-        acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], k4_f64_hi(((w[i] & 0x7fff0000u) >> 3) + kF64Rebias));
-      }
-      return;
-    }
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {  // zero, tiny or beyond-f16 element in the unit: convert
-      const uint32_t h = bf2_to_h2(w[i]) & 0x7fff7fffu;
-      acc[2 * i] = __dadd_rn(acc[2 * i], k4_f64_hi((__float_as_uint(lo_f(h)) >> 3) + kF64Rebias));
-      acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], k4_f64_hi((__float_as_uint(hi_f(h)) >> 3) + kF64Rebias));
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t h = w[i] & 0x7fff7fffu;
-      acc[2 * i] = __dadd_rn(acc[2 * i], k4_f64_hi((__float_as_uint(lo_f(h)) >> 3) + kF64Rebias));
-      acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], k4_f64_hi((__float_as_uint(hi_f(h)) >> 3) + kF64Rebias));
-    }
-  }
-}
-
-// 8 elements from shared staging (raw bf16 / f16 words; f32 converted to f16).
-template <int DT>
-__device__ __forceinline__ uint4 k4_lds(const unsigned char *p) {
-  if (DT == ADC_F32) {
-    const uint4 a = *reinterpret_cast<const uint4 *>(p), c = *reinterpret_cast<const uint4 *>(p + 16);
-    return make_uint4(f32x2_to_h2(__uint_as_float(a.x), __uint_as_float(a.y)),
-                      f32x2_to_h2(__uint_as_float(a.z), __uint_as_float(a.w)),
-                      f32x2_to_h2(__uint_as_float(c.x), __uint_as_float(c.y)),
-                      f32x2_to_h2(__uint_as_float(c.z), __uint_as_float(c.w)));
-  }
-  return *reinterpret_cast<const uint4 *>(p);
-}
-template <int DT>
-__device__ __forceinline__ uint4 k4_ldg(const void *x, int64_t e) {
-  if (DT == ADC_F32) return Loader<ADC_F32>::template load8<false>(x, e);
-  return Loader<ADC_F16>::template load8<false>(x, e);
-}
-// One element as f16 bits.
-template <int DT>
-__device__ __forceinline__ uint16_t k4_one(const unsigned char *p) {
-  if (DT == ADC_F32) return __half_as_ushort(__float2half_rn(*reinterpret_cast<const float *>(p)));
-  const uint16_t v = *reinterpret_cast<const uint16_t *>(p);
-  return DT == ADC_BF16 ? static_cast<uint16_t>(bf16_bits_to_f16_bits(v)) : v;
-}
-
-// Zero masks of 32 columns (16 words) from 32 flag bytes.
-__device__ __forceinline__ void k4_masks32(const uint8_t *flag32, uint32_t *mk) {
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    mk[4 * q] = mk[4 * q + 1] = mk[4 * q + 2] = mk[4 * q + 3] = 0xffffffffu;
-    zero_apply8(mk + 4 * q, *reinterpret_cast<const uint2 *>(flag32 + 8 * q));
-  }
-}
-
-// Bank-conflict-free reads of a lane's 64 contiguous shared-memory bytes:
-// lane i reads its four 16-byte units in the order u = (q + rot) % 4 with
-// rot = (i >> 1) & 3, so the 8 lanes of each 128-byte wavefront hit 8
-// distinct bank groups (unrotated, lanes 64 bytes apart collide 4-way).
-// Quantisation is per element and the abs-max is order-free, so the lane
-// works in rotated order; only the masks (once) and the four code words
-// (per quad) are permuted back.
-__device__ __forceinline__ uint32_t k4_rot_sel(const uint32_t *v, int u) {  // v[u], u in 0..3, no local memory
-  const uint32_t lo = (u & 1) ? v[1] : v[0], hi = (u & 1) ? v[3] : v[2];
-  return (u & 2) ? hi : lo;
-}
-__device__ __forceinline__ void k4_rotate_masks(uint32_t *mk, int rot) {  // mk[4q+i] <- mk[4((q+rot)%4)+i]
-  uint32_t r[16];
-#pragma unroll
-  for (int q = 0; q < 4; ++q)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t v[4] = {mk[i], mk[4 + i], mk[8 + i], mk[12 + i]};
-      r[4 * q + i] = k4_rot_sel(v, (q + rot) & 3);
-    }
-#pragma unroll
-  for (int i = 0; i < 16; ++i) mk[i] = r[i];
-}
-__device__ __forceinline__ uint4 k4_unrotate(uint4 cw, int rot) {  // word u of the result = cw[(u - rot) % 4]
-  const uint32_t v[4] = {cw.x, cw.y, cw.z, cw.w};
-  return make_uint4(k4_rot_sel(v, (4 - rot) & 3), k4_rot_sel(v, (5 - rot) & 3), k4_rot_sel(v, (6 - rot) & 3),
-                    k4_rot_sel(v, (7 - rot) & 3));
-}
-
-// Symmetric codes of one lane's 32 consecutive elements (16 raw words); the
-// group is spread over L4 aligned lanes (every lane of the warp calls).
-template <bool BF, int L4>
-__device__ __forceinline__ uint4 k4_quad_quant(const uint32_t *w, bool act, uint16_t &s_bits, bool &bad) {
+__device__ __noinline__ uint2 quant16_slow(uint4 a, uint4 c, uint32_t s_bits, bool native) {
   using R = Raw<BF ? ADC_BF16 : ADC_F16>;
-  uint32_t m = 0;
-  if (act) {
-#pragma unroll
-    for (int i = 0; i < 16; ++i) m = __vmaxu2(m, w[i] & 0x7fff7fffu);
-  }
-  m = warp_max_u2<L4>(m);
-  const uint32_t top = max(m & 0xffffu, m >> 16);
-  bool native = true;
-  if (BF) {
-    bad = top >= 0x4780u;     // >= 65536 rounds to f16 inf (also inf / NaN)
-    native = top >= 0x3900u;  // top >= 2^-13: tiny-value rounding is code-neutral
-    s_bits = sym_scale_bits(bf16_bits_to_f16_bits(top));
-  } else {
-    bad = top >= 0x7c00u;
-    s_bits = sym_scale_bits(top);
-  }
-  if (!act) return make_uint4(0, 0, 0, 0);  // (the exact path below is for real tiny groups only)
-  uint32_t t[32];
-  if ((!BF || native) && s_bits >= 0x0400u) {
-    // normal scale: correctly rounded h/s two lanes per FMUL2 / FFMA2
-    // (Markstein), RNE by the magic add, the upper clip in the saturating pack
-    const float sc = h2f(s_bits), inv = rcp_approx(sc);
-    const uint64_t inv2 = f2_pack(inv, inv), ns2 = f2_pack(-sc, -sc), mg2 = f2_pack(kMagic8, kMagic8);
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const uint64_t h2 = f2_pack(R::lo(w[i]), R::hi(w[i]));
-      const uint64_t r0 = f2_mul(h2, inv2);
-      const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
-      float tl, th;
-      f2_unpack(f2_add(r1, mg2), tl, th);
-      t[2 * i] = __float_as_uint(tl);
-      t[2 * i + 1] = __float_as_uint(th);
-    }
-  } else if (!BF || native) {
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  uint32_t t[16];
+  if (!BF || native) {
     const float s0 = h2f(s_bits), sc = s0 == 0.f ? 1.f : s0, inv = rcp_approx(sc);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
+    for (int i = 0; i < 8; ++i) {
       t[2 * i] = sym_tbits_clip2(R::lo(w[i]), sc, inv);
       t[2 * i + 1] = sym_tbits_clip2(R::hi(w[i]), sc, inv);
     }
   } else {
-    unit_codes_exact<BF, 16>(w, h2f(s_bits), 0.f, false, t);
+    unit_codes_exact<BF, 8>(w, h2f(s_bits), 0.f, false, t);
   }
-  return make_uint4(pack8_tbits_sat(t), pack8_tbits_sat(t + 8), pack8_tbits_sat(t + 16), pack8_tbits_sat(t + 24));
+  return make_uint2(pack8_tbits_sat(t), pack8_tbits_sat(t + 8));
 }
 
-// Grid barrier split in two so a CTA can work between its arrival and the
-// wait (thread 0 of each CTA; the CTA synchronises around them): one
-// non-returning release-add per CTA on a monotonic counter, then acquire
-// polls until it reaches target (wrap-safe).
-__device__ __forceinline__ void k4_grid_arrive(uint32_t *cnt) {
-  asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-}
-__device__ __forceinline__ void k4_grid_wait(const uint32_t *cnt, uint32_t target) {
-  while (static_cast<int32_t>(k4_ld_acquire(cnt) - target) < 0) {
+// Symmetric codes of a lane's 16 elements (raw words in load order; the
+// abs-max runs over ab = |w| & channel mask), the 128-group spread over 8
+// aligned lanes.  Every lane of the warp calls (lanes without data pass
+// zeros).  Codes of zeroed channels are not forced to 0 here (the caller ANDs
+// the code words): the abs-max alone decides the scale.
+template <bool BF>
+__device__ __forceinline__ uint2 quant16(const uint32_t *w, const uint32_t *ab, uint16_t &s_bits, bool &bad) {
+  using R = Raw<BF ? ADC_BF16 : ADC_F16>;
+  uint32_t m = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) m = __vmaxu2(m, ab[i]);
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  const uint32_t top = max(m & 0xffffu, m >> 16);
+  // fast: 2^-11 <= top < 65536 (bf16: the value IS f16(top); f16: finite):
+  // s = f16(top / 8) is a normal f16 (top / 8 is exact in f32)
+  const bool fast = BF ? (top - 0x3a00u < 0x4780u - 0x3a00u) : (top - 0x1000u < 0x7c00u - 0x1000u);
+  if (!fast) {
+    bool native = true;
+    if (BF) {
+      bad = top >= 0x4780u;     // >= 65536 rounds to f16 inf (also inf / NaN)
+      native = top >= 0x3900u;  // top >= 2^-13: tiny-value rounding is code-neutral
+      s_bits = sym_scale_bits(bf16_bits_to_f16_bits(top));
+    } else {
+      bad = top >= 0x7c00u;
+      s_bits = sym_scale_bits(top);
+    }
+    return quant16_slow<BF>(make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]), s_bits, native);
   }
+  bad = false;
+  const float topf = BF ? __uint_as_float(top << 16) : h2f(top);
+  s_bits = __half_as_ushort(__float2half_rn(topf * 0.125f));
+  // correctly rounded h/s two lanes per FMUL2 / FFMA2 (Markstein), RNE by the
+  // magic add, the clips in the saturating pack
+  const float sc = h2f(s_bits), inv = rcp_approx(sc);
+  const uint64_t inv2 = f2_pack(inv, inv), ns2 = f2_pack(-sc, -sc), mg2 = f2_pack(kMagic8, kMagic8);
+  uint32_t t[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t h2 = f2_pack(R::lo(w[i]), R::hi(w[i]));
+    const uint64_t r0 = f2_mul(h2, inv2);
+    const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
+    float tl, th;
+    f2_unpack(f2_add(r1, mg2), tl, th);
+    t[2 * i] = __float_as_uint(tl);
+    t[2 * i + 1] = __float_as_uint(th);
+  }
+  return make_uint2(pack8_tbits_sat(t), pack8_tbits_sat(t + 8));
+}
+
+// quant16 on precomputed f32 values of the unit (f[2i] / f[2i+1] = low /
+// high element of word i) and the lane's abs-max word mx.
+template <bool BF>
+__device__ __forceinline__ uint2 quant16f(const uint32_t *w, const float *f, uint32_t mx, uint16_t &s_bits,
+                                          bool &bad) {
+  uint32_t m = mx;
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 1));
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 2));
+  m = __vmaxu2(m, __shfl_xor_sync(0xffffffffu, m, 4));
+  const uint32_t top = max(m & 0xffffu, m >> 16);
+  const bool fast = BF ? (top - 0x3a00u < 0x4780u - 0x3a00u) : (top - 0x1000u < 0x7c00u - 0x1000u);
+  if (!fast) {
+    bool native = true;
+    if (BF) {
+      bad = top >= 0x4780u;
+      native = top >= 0x3900u;
+      s_bits = sym_scale_bits(bf16_bits_to_f16_bits(top));
+    } else {
+      bad = top >= 0x7c00u;
+      s_bits = sym_scale_bits(top);
+    }
+    return quant16_slow<BF>(make_uint4(w[0], w[1], w[2], w[3]), make_uint4(w[4], w[5], w[6], w[7]), s_bits, native);
+  }
+  bad = false;
+  const float topf = BF ? __uint_as_float(top << 16) : h2f(top);
+  s_bits = __half_as_ushort(__float2half_rn(topf * 0.125f));
+  const float sc = h2f(s_bits), inv = rcp_approx(sc);
+  const uint64_t inv2 = f2_pack(inv, inv), ns2 = f2_pack(-sc, -sc), mg2 = f2_pack(kMagic8, kMagic8);
+  uint32_t t[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint64_t h2 = f2_pack(f[2 * i], f[2 * i + 1]);
+    const uint64_t r0 = f2_mul(h2, inv2);
+    const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
+    float tl, th;
+    f2_unpack(f2_add(r1, mg2), tl, th);
+    t[2 * i] = __float_as_uint(tl);
+    t[2 * i + 1] = __float_as_uint(th);
+  }
+  return make_uint2(pack8_tbits_sat(t), pack8_tbits_sat(t + 8));
+}
+
+// Zero masks of 16 columns (8 words) from 16 flag bytes (0/1), in load order
+// (the half at +8*sw first).
+__device__ __forceinline__ void masks16(const uint8_t *flag16, int sw, uint32_t *mk) {
+  const uint4 f = *reinterpret_cast<const uint4 *>(flag16);
+  const uint2 h0 = sw ? make_uint2(f.z, f.w) : make_uint2(f.x, f.y);
+  const uint2 h1 = sw ? make_uint2(f.x, f.y) : make_uint2(f.z, f.w);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) mk[i] = 0xffffffffu;
+  zero_apply8(mk, h0);
+  zero_apply8(mk + 4, h1);
+}
+
+// Code-word nibble masks of the 8 zero masks (0xF where the channel is kept).
+__device__ __forceinline__ uint2 nibble_masks(const uint32_t *mk) {
+  uint32_t c[2] = {0u, 0u};
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if ((mk[j >> 1] >> (16 * (j & 1))) & 1u) c[j >> 3] |= 0xfu << (4 * (j & 7));
+  return make_uint2(c[0], c[1]);
+}
+
+// One row-unit: optional column sums, quantise with mask mk, store the codes
+// (in column order) and the group's scale.  Every lane of the warp calls; act
+// = this lane holds a row (a group's 8 lanes agree).
+struct Unit {
+  int sw;
+  bool leader;  // lane 0 of the 8-lane group
+};
+// outputs of the quantiser (passed by value to out-of-line helpers: a
+// reference to the kernel's parameter block would copy it to local memory)
+struct QOut {
+  uint8_t *codes;
+  uint16_t *scales;
+  uint32_t *err;
+};
+
+// Column sums of one unit on the slow path (a zero, a tiny bf16 value, or a
+// predicted-outlier lane): h = f16(x) -> f32 -> float64, exactly numpy's
+// astype(float16) then float64.
+template <bool BF>
+__device__ __forceinline__ void colsum16_slow(double *acc, uint4 v0, uint4 v1) {
+  const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const uint32_t h = (BF ? bf2_to_h2(w[i]) : w[i]) & 0x7fff7fffu;
+    acc[2 * i] = __dadd_rn(acc[2 * i], static_cast<double>(lo_f(h)));
+    acc[2 * i + 1] = __dadd_rn(acc[2 * i + 1], static_cast<double>(hi_f(h)));
+  }
+}
+
+// One row-unit (16 elements of a row in load order): column |h| sums (SUM)
+// and the group's symmetric codes with the zero mask mk; stores the codes
+// (column order) and the group's scale.  Every lane of the warp calls; act =
+// this lane holds a row (a group's 8 lanes agree).
+//   sums: bf16 values in [2^-17, 65536) ARE their f16 rounding, so |x| as
+//   f32 -> float64 (F2F) is exact; f16 values always convert exactly.  The
+//   same f32 values feed the quotients.
+template <bool BF, bool SUM, bool QUANT = true>
+__device__ __forceinline__ void row_unit(const Unit &U, bool act, uint4 v0, uint4 v1, const uint32_t *mk, uint2 cm,
+                                         double *acc, uint2 *code_dst, uint16_t *scale_dst, uint32_t *err) {
+  using R = Raw<BF ? ADC_BF16 : ADC_F16>;
+  const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+  uint32_t mx = 0, mn = 0xffffffffu;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    mx = __vmaxu2(mx, w[i] & mk[i] & 0x7fff7fffu);                  // abs-max of the kept channels
+    if (SUM && BF) mn = __vminu2(mn, w[i] & 0x7fff7fffu);            // abs-min of all channels
+  }
+  float f[16];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    f[2 * i] = R::lo(w[i]);
+    f[2 * i + 1] = R::hi(w[i]);
+  }
+  if (SUM && act) {
+    // bf16: a unit holding a zero or a value below 2^-17 (any channel) takes
+    // the converting path
+    if (!BF || min(mn & 0xffffu, mn >> 16) >= 0x3700u) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = __dadd_rn(acc[j], static_cast<double>(fabsf(f[j])));
+    } else {
+      colsum16_slow<BF>(acc, v0, v1);
+    }
+  }
+  if (!QUANT) return;
+  uint16_t s_bits;
+  bool bad;
+  uint2 cw = quant16f<BF>(w, f, mx, s_bits, bad);
+  if (!act) return;
+  cw.x &= cm.x;
+  cw.y &= cm.y;
+  *code_dst = U.sw ? make_uint2(cw.y, cw.x) : cw;
+  if (U.leader) {
+    *scale_dst = s_bits;
+    if (bad) raise_err(err, ADC_ERR_NONFINITE);
+  }
+}
+
+// A, the flagged-channel side buffer under the prediction: one warp copies
+// the predicted outlier columns of a resident chunk (cr rows) from shared
+// memory to val[rank][row] (codec.py:339-340).  Consecutive lanes take
+// consecutive rows of one column, so every store instruction writes whole
+// 32-byte sectors.
+template <bool BF>
+__device__ __noinline__ void capture_chunk(const unsigned char *chunk, int rowb, int cr, int tc0, const uint16_t *ptcol,
+                                           int ntp, int rank0, int64_t row0, int64_t rows, int64_t k_cap, uint16_t *val,
+                                           uint32_t *err) {
+  const int lane = threadIdx.x & 31;
+  bool bad = false;
+  for (int it = lane; it < ntp * cr; it += 32) {
+    const int j = it / cr, r = it - j * cr;
+    const int rank = rank0 + j;
+    const uint32_t v = *reinterpret_cast<const uint16_t *>(chunk + r * rowb + (ptcol[j] - tc0) * 2);
+    const uint32_t h = BF ? bf16_bits_to_f16_bits(v) : v;
+    bad |= (h & 0x7fffu) >= 0x7c00u;
+    if (rank < k_cap) val[static_cast<int64_t>(rank) * rows + row0 + r] = static_cast<uint16_t>(h);
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) raise_err(err, ADC_ERR_NONFINITE);
+}
+
+// D, out of line: re-quantise the lane's unit in every row of the tile with
+// the actual channel set (from shared memory when resident, else global).
+template <bool BF>
+__device__ __noinline__ void redo_rows(QOut q, const uint16_t *x, int64_t cols, int CR, int slot_bytes, Unit U,
+                                       bool redo, uint4 mk0, uint4 mk1, const unsigned char *slots, bool resident,
+                                       int64_t r0, int nrows, int W, int p, int P, int u, int tc0) {
+  const uint32_t mk[8] = {mk0.x, mk0.y, mk0.z, mk0.w, mk1.x, mk1.y, mk1.z, mk1.w};
+  const uint2 cm = nibble_masks(mk);
+#pragma unroll 1
+  for (int base = 0; base < nrows; base += P) {  // warp-uniform trip count
+    const int rr = base + p;
+    const bool act = redo && rr < nrows;
+    const int64_t e = (r0 + rr) * cols + tc0 + 16 * u;
+    uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+    if (!act) {
+    } else if (resident) {
+      const int c = rr / CR;
+      const unsigned char *src = slots + c * slot_bytes + (rr - c * CR) * W * 2 + 32 * u;
+      v0 = *reinterpret_cast<const uint4 *>(src + 16 * U.sw);
+      v1 = *reinterpret_cast<const uint4 *>(src + 16 * (1 - U.sw));
+    } else {
+      const uint4 *src = reinterpret_cast<const uint4 *>(x + e);
+      v0 = __ldcg(src + U.sw);
+      v1 = __ldcg(src + 1 - U.sw);
+    }
+    row_unit<BF, false>(U, act, v0, v1, mk, cm, nullptr, reinterpret_cast<uint2 *>(q.codes + e / 2),
+                        q.scales + (e >> 7), q.err);
+  }
+}
+
+// numpy pairwise sum over the S[] terms (squared deviations when `mean` is
+// given): leaves by 8-lane groups (the 8 interleaved accumulators of a
+// 128-block), internal nodes level by level by warp 0.  Every thread calls;
+// all receive 0.0 + sum.
+__device__ __noinline__ double tree_sum(const OTree &tr, const double *S, bool squared, double mean, double *s_tv,
+                                        double *s_out) {
+  const int tid = threadIdx.x, lane = tid & 31, j8 = tid & 7;
+  constexpr int ng = kOT / 8;
+  for (int g0 = 0; g0 < tr.n_leaves; g0 += ng) {
+    const int g = g0 + (tid >> 3);
+    const bool valid = g < tr.n_leaves;
+    const int lo = valid ? tr.leaf_lo[g] : 0, m = valid ? tr.leaf_n[g] : 0;
+    const int stop = m - (m % 8);
+    double r = 0.0;
+    if (valid && m >= 8) {
+      for (int i = j8; i < stop; i += 8) {
+        double v = S[lo + i];
+        if (squared) {
+          const double d = __dsub_rn(v, mean);
+          v = __dmul_rn(d, d);
+        }
+        r = i == j8 ? v : __dadd_rn(r, v);
+      }
+    }
+    // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7))
+    const double x1 = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1, 8));
+    const double x2 = __dadd_rn(x1, __shfl_down_sync(0xffffffffu, x1, 2, 8));
+    double x3 = __dadd_rn(x2, __shfl_down_sync(0xffffffffu, x2, 4, 8));
+    if (valid && j8 == 0) {
+      if (m < 8) x3 = 0.0;
+      for (int i = stop; i < m; ++i) {
+        double v = S[lo + i];
+        if (squared) {
+          const double d = __dsub_rn(v, mean);
+          v = __dmul_rn(d, d);
+        }
+        x3 = __dadd_rn(x3, v);
+      }
+      s_tv[g] = x3;
+    }
+  }
+  __syncthreads();
+  if (tid < 32) {
+    const int nl = tr.n_leaves;
+    int beg = 0;
+    for (int h = 0; h < tr.n_levels; ++h) {
+      const int end = tr.level_end[h];
+      for (int q = beg + lane; q < end; q += 32) s_tv[nl + q] = __dadd_rn(s_tv[tr.left[q]], s_tv[tr.right[q]]);
+      __syncwarp();
+      beg = end;
+    }
+    if (lane == 0) *s_out = __dadd_rn(0.0, s_tv[beg == 0 ? 0 : nl + beg - 1]);
+  }
+  __syncthreads();
+  return *s_out;
 }
 
 // numpy row-order column sums (only when some column total reaches 2^29):
 // the columns shared out over the grid, one thread per column.
-template <int DT>
-__device__ __noinline__ void k4_numpy_order_sums(const void *x, int64_t rows, int64_t cols, double *out) {
-  constexpr int EB = DT == ADC_F32 ? 4 : 2;
-  for (int64_t c = static_cast<int64_t>(blockIdx.x) * kK4T + threadIdx.x; c < cols;
-       c += static_cast<int64_t>(gridDim.x) * kK4T) {
+template <bool BF>
+__device__ __noinline__ void numpy_order_sums(const uint16_t *x, int64_t rows, int64_t cols, double *out) {
+  for (int64_t c = static_cast<int64_t>(blockIdx.x) * kOT + threadIdx.x; c < cols;
+       c += static_cast<int64_t>(gridDim.x) * kOT) {
     double sum = 0.0;
+#pragma unroll 1
     for (int64_t r = 0; r < rows; ++r) {
-      const unsigned char *px = static_cast<const unsigned char *>(x) + (r * cols + c) * EB;
-      sum = __dadd_rn(sum, fabs(static_cast<double>(h2f(k4_one<DT>(px)))));
+      const uint32_t v = x[r * cols + c];
+      const uint32_t h = BF ? bf16_bits_to_f16_bits(v) : v;
+      sum = __dadd_rn(sum, fabs(static_cast<double>(h2f(h))));
     }
     __stcg(out + c, sum);
   }
 }
 
-// Error path only (k beyond the side buffer): the flagged channels that were
-// not gathered are still checked for the float16 overflow of codec.py:167-170.
-template <int DT>
-__device__ __noinline__ void k4_check_ungathered(const void *x, int64_t cols, int64_t r0, int nrows,
-                                                 const uint8_t *s_flag, int64_t ke, int64_t k, uint32_t *err) {
-  constexpr int EB = DT == ADC_F32 ? 4 : 2;
-  const int64_t items = (k - ke) * nrows;
-  for (int64_t it = threadIdx.x; it < items; it += kK4T) {
-    const int64_t rank = ke + it / nrows, rr = it % nrows;
-    int64_t cc = -1;
-    for (int64_t q = 0, seen = 0; q < cols; ++q)  // rank -> column (slow, error path)
-      if (s_flag[q] && seen++ == rank) {
-        cc = q;
-        break;
-      }
-    if (cc < 0) continue;
-    const unsigned char *src = static_cast<const unsigned char *>(x) + ((r0 + rr) * cols + cc) * EB;
-    if ((k4_one<DT>(src) & 0x7fffu) >= 0x7c00u) raise_err(err, ADC_ERR_NONFINITE);
+// E: the flagged channels of the tile, rows [r0, r0 + nrows): val[rank][r] = f16(x[r, col]).
+template <bool BF>
+__device__ __noinline__ void side_buffer(const uint16_t *x, int64_t rows, int64_t cols, int CR, int slot_bytes,
+                                         int64_t k_cap, uint16_t *val, uint32_t *err, const unsigned char *slots,
+                                         bool resident, int64_t r0, int nrows, int W, int tc0, const uint16_t *s_tcol,
+                                         int nt, int rank0) {
+  const int items = nt * nrows;
+#pragma unroll 1
+  for (int it = threadIdx.x; it < items; it += kOT) {
+    const int j = it / nrows, rr = it - j * nrows;
+    const int rank = rank0 + j;
+    const int cc = s_tcol[j];
+    uint32_t v;
+    if (resident) {
+      const int c = rr / CR;
+      v = *reinterpret_cast<const uint16_t *>(slots + c * slot_bytes + (rr - c * CR) * W * 2 + (cc - tc0) * 2);
+    } else {
+      v = __ldcg(x + (r0 + rr) * cols + cc);
+    }
+    const uint32_t h = BF ? bf16_bits_to_f16_bits(v) : v;
+    if ((h & 0x7fffu) >= 0x7c00u) raise_err(err, ADC_ERR_NONFINITE);
+    if (rank < k_cap) val[static_cast<int64_t>(rank) * rows + r0 + rr] = static_cast<uint16_t>(h);
   }
 }
 
-template <int DT, int L4, int J, bool SPEC>
-__global__ void __launch_bounds__(kK4T, 1) outlier_k4(K4Args a) {
+template <bool BF>
+__global__ void __launch_bounds__(kOT, 1) outlier_onepass(OArgs a) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ __align__(8) uint64_t s_full[kK4MaxSlots];
-  __shared__ uint32_t s_done[kK4MaxSlots];
-  __shared__ double s_red[32];
-  __shared__ double s_tv[2 * kK4MaxLeaves];
-  __shared__ double s_stat[4];
-  __shared__ int s_int[72];
-  __shared__ uint32_t s_ctl[4];
-  constexpr bool BF = DT == ADC_BF16;
-  constexpr int EB = DT == ADC_F32 ? 4 : 2;  // input bytes per element
+  __shared__ __align__(8) uint64_t s_full[kOMaxSlots];
+  __shared__ uint32_t s_done[kOMaxSlots];
+  __shared__ __align__(8) uint64_t s_pbar;  // the prediction's copy
+  __shared__ double s_red[kOW];
+  __shared__ double s_tv[2 * kOMaxLeaves];
+  __shared__ double s_stat;
+  __shared__ int s_cnt[kOW + 2];
+  __shared__ int s_lt[kOW], s_lt1[kOW];
+  __shared__ uint32_t s_ctl[3];
+  __shared__ uint16_t s_tcol[kOStripCols];  // flagged columns of this strip, ascending
+  __shared__ OTree s_tree;
+  __shared__ uint16_t s_urank[kOMaxLeaves * 8 + 1];  // predicted flags before each 16-column unit (+ total)
+  __shared__ uint16_t s_ptcol[kOStripCols];           // predicted outlier columns of the strip, ascending
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t C = gridDim.x;
   const int b = blockIdx.x;
   const long long t_0 = clock64();
-  if (a.trace && lane == 0 && b < kK4TraceCtas) {
+  if (a.trace && lane == 0 && b < kOTraceCtas) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    if (tid == 0) g_k4trace[b * kK4TraceSlots] = gt;
-    g_k4trace[b * kK4TraceSlots + 32 + wid] = gt;
+    if (tid == 0) g_k4trace[b * kOTraceSlots] = gt;
+    g_k4trace[b * kOTraceSlots + 32 + wid] = gt;
   }
   const int64_t rows = a.rows, cols = a.cols;
-  const int ucols = a.ucols, P = a.P, Q = a.Q, P2 = a.P2;
-  const int row_bytes = static_cast<int>(cols) * EB;  // <= 64 KB
+  // this CTA's tile: strip columns [tc0, tc0 + W), slab rows [r0, r1)
+  const int strip = b % a.strips, slab = b / a.strips;
+  const int G = static_cast<int>(cols >> 7);
+  const int g0 = G * strip / a.strips, g1 = G * (strip + 1) / a.strips;
+  const int tc0 = 128 * g0, W = 128 * (g1 - g0);
+  const int64_t r0 = static_cast<int64_t>(slab) * a.rbase + min(slab, a.rrem);
+  const int nrows = a.rbase + (slab < a.rrem ? 1 : 0);
   const int CR = a.chunk_rows;
-
-  // shared carve-up (the host computes the same sizes)
-  const int n_slots = a.n_res + a.n_ring;
-  unsigned char *slots = smem;
-  double *S = reinterpret_cast<double *>(smem + n_slots * a.slot_bytes);
-  uint8_t *s_flag = reinterpret_cast<uint8_t *>(S + cols);                               // cols + 16
-  uint32_t *s_idx = reinterpret_cast<uint32_t *>(s_flag + ((cols + 16 + 15) & ~15ll));   // cols / 2 + 1
-
-  // this CTA's slab: rows [r0, r1) in chunks of CR rows
-  const int64_t r0 = rows * b / C, r1 = rows * (b + 1) / C;
-  const int nrows = static_cast<int>(r1 - r0);
   const int nchunks = (nrows + CR - 1) / CR;
-  const char *xslab = static_cast<const char *>(a.x) + r0 * row_bytes;
-  auto slot_of = [&](int c) { return c < a.n_res ? c : a.n_res + (c - a.n_res) % a.n_ring; };
-  auto issue = [&](int c) {  // one thread
-    const int s = slot_of(c);
+  const bool resident = nchunks <= a.n_slots;
+  unsigned char *slots = smem;
+  double *S = reinterpret_cast<double *>(smem + a.stats_off);  // [cols]
+  uint8_t *s_flag = reinterpret_cast<uint8_t *>(S + cols);     // [cols + 16]
+  uint8_t *s_pred = smem + a.pred_off;                          // [cols + 16] previous call's flags
+
+  const int rowb = W * 2;
+  auto issue = [&](int c) {  // warp-cooperative: lane i copies rows i, i + 32, ... of chunk c
+    const int s = c % a.n_slots;
     const int cr = min(CR, nrows - c * CR);
-    const uint32_t bytes = static_cast<uint32_t>(cr * row_bytes);
-    mbar_expect_tx(&s_full[s], bytes);
-    const void *src = xslab + static_cast<int64_t>(c) * CR * row_bytes;
+    if (lane == 0) mbar_expect_tx(&s_full[s], static_cast<uint32_t>(cr * rowb));
+    __syncwarp();
     unsigned char *dst = slots + s * a.slot_bytes;
-    if (c >= a.n_res && a.keep) {
-      asm volatile(
-          "{\n\t.reg .b64 pol;\n\t"
-          "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], pol;\n\t}"
-          ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(&s_full[s]))
-          : "memory");
+    const uint16_t *src = a.x + (r0 + static_cast<int64_t>(c) * CR) * cols + tc0;
+    if (W == cols) {  // contiguous rows: one copy
+      if (lane == 0) bulk_g2s(dst, src, static_cast<uint32_t>(cr * rowb), &s_full[s]);
     } else {
-      bulk_g2s(dst, src, bytes, &s_full[s]);
+      for (int i = lane; i < cr; i += 32) bulk_g2s(dst + i * rowb, src + i * cols, static_cast<uint32_t>(rowb), &s_full[s]);
     }
   };
-  if (tid == 0) {
-    for (int s = 0; s < n_slots; ++s) {
-      mbar_init(&s_full[s], 1);
-      s_done[s] = 0;
-    }
-    fence_barrier_init();
-  }
-  __syncthreads();
-  if (tid == 0) {
-    for (int c = 0; c < min(nchunks, n_slots); ++c) issue(c);
-  } else if (tid == 32) {  // consumed after phase A
-    s_ctl[0] = a.ctl[1];   // barrier base
-    s_ctl[1] = a.ctl[2];   // epoch
-    s_ctl[2] = a.ctl[3];   // cols of the last call (accumulator layout)
-  }
-  // sum mapping.  J == 1: a warp covers U = 32 / P unit columns x P row lanes
-  // (8 consecutive units per 128-byte wavefront: conflict-free LDS.128; the
-  // row lanes fold with xor shuffles).  J > 1: unit columns tid + j * kK4T.
-  const int U = 32 / P;
-  const int p = (J == 1) ? lane / U : 0;
-  int ucj[J];
-  bool onj[J];
-#pragma unroll
-  for (int j = 0; j < J; ++j) {
-    ucj[j] = (J == 1) ? wid * U + (lane - p * U) : tid + j * kK4T;
-    onj[j] = ucj[j] < ucols;
-  }
-  // quantise mapping: thread (p2, q): 32 columns [32 q, 32 q + 32) of rows p2, p2 + P2, ...
-  const int p2 = tid / Q, qd = tid - p2 * Q;
-  const bool qon = p2 < P2;
-  const int rot = EB == 4 ? (lane & 3) : ((lane >> 1) & 3);  // see k4_rot_sel
-  // predicted zero masks (previous call's flags) for the quantise mapping
-  uint32_t pmk[16];
-  if (SPEC) {
-    if (qon) {
-      const uint4 f0 = *reinterpret_cast<const uint4 *>(a.pflag + 32 * qd);
-      const uint4 f1 = *reinterpret_cast<const uint4 *>(a.pflag + 32 * qd + 16);
-      const uint32_t fw[8] = {f0.x, f0.y, f0.z, f0.w, f1.x, f1.y, f1.z, f1.w};
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        pmk[4 * q] = pmk[4 * q + 1] = pmk[4 * q + 2] = pmk[4 * q + 3] = 0xffffffffu;
-        zero_apply8(pmk + 4 * q, make_uint2(fw[2 * q], fw[2 * q + 1]));
+  if (wid == 0) {  // barriers, then every copy: the prediction first, the chunks behind it
+    if (lane == 0) {
+#pragma unroll 1
+      for (int s = 0; s < a.n_slots; ++s) {
+        mbar_init(&s_full[s], 1);
+        s_done[s] = 0;
       }
-      k4_rotate_masks(pmk, rot);
-    } else {
-#pragma unroll
-      for (int i = 0; i < 16; ++i) pmk[i] = 0u;
+      mbar_init(&s_pbar, 1);
+      fence_barrier_init();
+      const uint32_t pbytes = static_cast<uint32_t>((cols + 15) & ~15ll);
+      mbar_expect_tx(&s_pbar, pbytes);
+      bulk_g2s(s_pred, a.pflag, pbytes, &s_pbar);
     }
+    __syncwarp();
+    K4TRACE(14);
+    for (int c = 0; c < min(nchunks, a.n_slots); ++c) issue(c);
+    K4TRACE(15);
+  } else if (tid == 32) {
+    s_ctl[0] = a.ctl[1];  // barrier base
+    s_ctl[1] = a.ctl[2];  // epoch
+    s_ctl[2] = a.ctl[3];  // cols of the last call (accumulator layout)
+  } else if (wid == 2) {  // the pairwise tree, for the statistics
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(&a.tree);
+    uint32_t *dst = reinterpret_cast<uint32_t *>(&s_tree);
+    for (int i = lane; i < static_cast<int>(sizeof(OTree) / 4); i += 32) dst[i] = src[i];
   }
-  uint32_t *codes = a.codes;
-  uint16_t *scales = a.scales;
-  const int trips1 = (CR + P - 1) / P, trips2 = (CR + P2 - 1) / P2;
-  // quantise chunk c (rows [c*CR, c*CR + cr) of the slab) with zero masks mk
-  // (rotated); from shared memory when resident, else from global (L2)
-  auto quant_chunk = [&](int c, const uint32_t *mk, bool on) {
-    const int cr = min(CR, nrows - c * CR);
-    const bool res = c < a.n_res;
-    const unsigned char *chunk = slots + slot_of(c) * a.slot_bytes;
-    const int qoff = 32 * qd * EB;
-    for (int i = 0; i < trips2; ++i) {
-      const int rr = p2 + i * P2;
-      const bool act = on && qon && rr < cr;
-      if (!__any_sync(0xffffffffu, act)) continue;  // warp-uniform
-      const int64_t e = (r0 + c * CR + rr) * cols + 32 * qd;  // first element of the quad
-      uint32_t w[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int u = (q + rot) & 3;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (act) v = res ? k4_lds<DT>(chunk + rr * row_bytes + qoff + 8 * u * EB) : k4_ldg<DT>(a.x, e + 8 * u);
-        w[4 * q] = v.x & mk[4 * q];
-        w[4 * q + 1] = v.y & mk[4 * q + 1];
-        w[4 * q + 2] = v.z & mk[4 * q + 2];
-        w[4 * q + 3] = v.w & mk[4 * q + 3];
-      }
-      uint16_t s_bits;
-      bool bad;
-      const uint4 cw = k4_unrotate(k4_quad_quant<BF, L4>(w, act, s_bits, bad), rot);
-      if (act) {
-        *reinterpret_cast<uint4 *>(codes + e / 8) = cw;
-        if ((qd & (L4 - 1)) == 0) {
-          scales[e / (32 * L4)] = s_bits;
-          if (bad) raise_err(a.err, ADC_ERR_NONFINITE);
-        }
-      }
+  __syncthreads();  // barrier initialisation visible to every warp
+  // the prediction (previous call's flags, in shared memory): exclusive counts per 16-column unit
+  {
+    const int gu = static_cast<int>(cols / 16);
+    int cnt0 = 0, cnt1 = 0;
+    mbar_wait(&s_pbar, 0);
+    if (2 * tid < gu) {
+      const uint4 f = *reinterpret_cast<const uint4 *>(s_pred + 32 * tid);
+      cnt0 = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);  // bytes are 0 / 1
     }
-  };
+    if (2 * tid + 1 < gu) {
+      const uint4 f = *reinterpret_cast<const uint4 *>(s_pred + 32 * tid + 16);
+      cnt1 = __popc(f.x) + __popc(f.y) + __popc(f.z) + __popc(f.w);
+    }
+    const int mine = cnt0 + cnt1;
+    int incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (lane == 31) s_cnt[wid] = incl;
+    __syncthreads();
+    int before = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kOW; ++w2) before += w2 < wid ? s_cnt[w2] : 0;
+    const int excl = before + incl - mine;
+    if (tid == kOT - 1) s_urank[gu] = static_cast<uint16_t>(excl + mine);  // (gu <= 1024 = 2 * kOT)
+    if (2 * tid < gu) s_urank[2 * tid] = static_cast<uint16_t>(excl);
+    if (2 * tid + 1 < gu) s_urank[2 * tid + 1] = static_cast<uint16_t>(excl + cnt0);
+    __syncthreads();
+  K4TRACE(18);
+  }
+  const QOut qo{a.codes, a.scales, a.err};
+  // lane mapping: thread (p, u), u = unit of 16 columns of the strip
+  const int units = W / 16;
+  const int P = kOT / units;
+  const int p = tid / units, u = tid - p * units;
+  const bool on = p < P;
+  Unit U;
+  U.sw = (u >> 2) & 1;  // 16-byte halves swapped on lanes 4..7 mod 8: conflict-free LDS.128
+  U.leader = (u & 7) == 0;
+  uint32_t pmk[8];  // predicted zero masks (previous call's flags), load order
+  uint32_t predm = 0;  // predicted outlier columns of the lane (bit j = column 16u + j)
+  int prank = 0;       // predicted rank of the first of them
+  if (on) {
+    masks16(s_pred + tc0 + 16 * u, U.sw, pmk);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) predm |= static_cast<uint32_t>(s_pred[tc0 + 16 * u + j]) << j;
+    prank = s_urank[tc0 / 16 + u];
+    if (p == 0)  // the strip's predicted columns, for the chunk captures
+      for (uint32_t m = predm; m; m &= m - 1) {
+        const int j = __ffs(m) - 1;
+        s_ptcol[prank - s_urank[tc0 / 16] + __popc(predm & ((1u << j) - 1u))] = static_cast<uint16_t>(tc0 + 16 * u + j);
+      }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) pmk[i] = 0xffffffffu;
+  }
+  K4TRACE(16);
+  const uint2 pcm = nibble_masks(pmk);
+  __syncthreads();  // s_ptcol
+  const int ptc0 = s_urank[tc0 / 16];
+  const int ntp = s_urank[(tc0 + W) / 16] - ptc0;  // predicted outlier columns in the strip
   K4TRACE(9);
 
-  // ---- A: column sums, chunk by chunk (SPEC: ring chunks also quantised now)
-  double acc[J][8];
+  // ---- A: column sums + quantisation with the predicted channel set ---------
+  double acc[16];
 #pragma unroll
-  for (int j = 0; j < J; ++j)
-#pragma unroll
-    for (int q = 0; q < 8; ++q) acc[j][q] = 0.0;
-  for (int c = 0; c < nchunks; ++c) {
-    const int s = slot_of(c);
-    const int cr = min(CR, nrows - c * CR);
-    const unsigned char *chunk = slots + s * a.slot_bytes;
-    mbar_wait(&s_full[s], (c < a.n_res ? 0 : (c - a.n_res) / a.n_ring) & 1);
-#pragma unroll
-    for (int j = 0; j < J; ++j) {
-      if (!onj[j]) continue;
-      const unsigned char *src = chunk + p * row_bytes + ucj[j] * 8 * EB;
-      for (int rr = p; rr < cr; rr += P, src += P * row_bytes) {
-        const uint4 v = k4_lds<DT>(src);
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-        k4_colsum8<BF>(acc[j], w);
+  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  {
+    // per-thread constants of the row walk: shared source offset (unit u, its
+    // swap), code / scale destinations of row p of chunk 0, strides per P rows
+    const int sm_off = p * rowb + 32 * u;
+    const int64_t e_first = (r0 + p) * cols + tc0 + 16 * u;
+    uint2 *cdst0 = reinterpret_cast<uint2 *>(a.codes) + e_first / 16;
+    uint16_t *sdst0 = a.scales + (e_first >> 7);
+    const int64_t cstep = static_cast<int64_t>(P) * cols / 16, sstep = static_cast<int64_t>(P) * cols / 128;
+    const int64_t cchunk = static_cast<int64_t>(CR) * cols / 16, schunk = static_cast<int64_t>(CR) * cols / 128;
+    int s = 0;
+    uint32_t phase = 0;
+    for (int c = 0; c < nchunks; ++c) {
+      const int cr = min(CR, nrows - c * CR);
+      mbar_wait(&s_full[s], phase);
+      if (wid == (c & (kOW - 1)) && ntp > 0 && a.val)
+        capture_chunk<BF>(slots + s * a.slot_bytes, rowb, cr, tc0, s_ptcol, ntp, ptc0,
+                          r0 + static_cast<int64_t>(c) * CR, rows, a.k_cap, a.val, a.err);
+      const unsigned char *src = slots + s * a.slot_bytes + sm_off;
+      uint2 *cdst = cdst0;
+      uint16_t *sdst = sdst0;
+      for (int rr = p; rr - p < cr; rr += P) {  // warp-uniform trip count
+        const bool act = on && rr < cr;
+        uint4 v0 = make_uint4(0, 0, 0, 0), v1 = v0;
+        if (act) {
+          v0 = *reinterpret_cast<const uint4 *>(src + 16 * U.sw);
+          v1 = *reinterpret_cast<const uint4 *>(src + 16 * (1 - U.sw));
+        }
+        row_unit<BF, true>(U, act, v0, v1, pmk, pcm, acc, cdst, sdst, a.err);
+        src += P * rowb;
+        cdst += cstep;
+        sdst += sstep;
       }
-    }
-    if (c >= a.n_res) {  // ring chunk: its slot is recycled
-      if (SPEC) quant_chunk(c, pmk, true);
-      __syncwarp();
-      if (lane == 0) {  // the last warp done refills the slot
-        const uint32_t d = atomicAdd(&s_done[s], 1u);
-        if (d == kK4Warps - 1) {
-          s_done[s] = 0;
-          if (c + a.n_ring < nchunks) {
+      cdst0 += cchunk;
+      sdst0 += schunk;
+      if (!resident) {  // ring: the last warp done with the slot refills it
+        __syncwarp();
+        uint32_t d = 0;
+        if (lane == 0) d = atomicAdd(&s_done[s], 1u);
+        d = __shfl_sync(0xffffffffu, d, 0);
+        if (d == kOW - 1) {
+          if (lane == 0) s_done[s] = 0;
+          if (c + a.n_slots < nchunks) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(c + a.n_ring);
+            issue(c + a.n_slots);
           }
         }
+      }
+      if (++s == a.n_slots) {
+        s = 0;
+        phase ^= 1u;
       }
     }
   }
   K4TRACE(1);
+  if (a.dbg == 1) return;
 
-  // ---- B: fold the row lanes (xor shuffles), one bulk reduction into the
-  // global sums, barrier arrival
+  // ---- B: fold the row lanes, one bulk reduction, barrier arrival ----------
+  // stage: row lane p's partial of column 16u + j at T[p * units + u][j], 17
+  // doubles per unit (the pad keeps lanes' 128-byte runs on distinct banks);
+  // the staging area is the statistics area (streamed tiles: the free ring).
+  __syncthreads();
+  K4TRACE(17);
+  double *T = S;  // P * units * 17 doubles
+  if (on) {
+    double *t = T + (p * units + u) * 17;
 #pragma unroll
-  for (int j = 0; j < J; ++j) {
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      double v = acc[j][k];
-      for (int o = U; o < 32; o <<= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
-      acc[j][k] = v;
-    }
-    if (p == 0 && onj[j]) {
-      double2 *d = reinterpret_cast<double2 *>(S + 8 * ucj[j]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) d[k] = make_double2(acc[j][2 * k], acc[j][2 * k + 1]);
+    for (int j = 0; j < 8; ++j) {
+      t[8 * U.sw + j] = acc[j];
+      t[8 * (1 - U.sw) + j] = acc[8 + j];
     }
   }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  K4TRACE(2);
   const uint32_t bar_base = s_ctl[0], epoch = s_ctl[1];
   const bool relayout = s_ctl[2] != static_cast<uint32_t>(cols);
   double *sacc = a.sacc + (epoch & 1u) * cols;
@@ -579,65 +772,57 @@ __global__ void __launch_bounds__(kK4T, 1) outlier_k4(K4Args a) {
   uint32_t n_bar = 0;
   if (relayout) {
     // first call on this workspace layout: zero the accumulator behind an extra barrier
-    for (int64_t c = static_cast<int64_t>(b) * kK4T + tid; c < cols; c += static_cast<int64_t>(C) * kK4T)
+    for (int64_t c = static_cast<int64_t>(b) * kOT + tid; c < cols; c += static_cast<int64_t>(C) * kOT)
       __stcg(sacc + c, 0.0);
     __threadfence();
-    __syncthreads();
     ++n_bar;
-    if (tid == 0) {
-      k4_grid_arrive(a.ctl);
-      k4_grid_wait(a.ctl, bar_base + n_bar * C);
-    }
-    __syncthreads();
+    cta_grid_sync(a.ctl, bar_base + n_bar * C);
   }
+  // the strip's column partials straight into the global accumulator (f64
+  // reductions in L2, exact: order-free); no async-proxy hand-off (its fence
+  // would wait for every code store of phase A)
+#pragma unroll 1
+  for (int c = tid; c < W; c += kOT) {
+    const double *t = T + (c >> 4) * 17 + (c & 15);
+    double v = t[0];
+#pragma unroll 4
+    for (int q = 1; q < P; ++q) v = __dadd_rn(v, t[q * units * 17]);
+    if (nrows > 0) atomicAdd(sacc + tc0 + c, v);
+  }
+  __syncthreads();
+  K4TRACE(2);
   ++n_bar;
-  if (tid == 0) {
-    if (nrows > 0) {
-      asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(sacc),
-                   "r"(smem_addr(S)), "r"(static_cast<uint32_t>(cols * 8))
-                   : "memory");
-      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-    }
-    k4_grid_arrive(a.ctl);
-  }
-  // SPEC: the resident chunks are quantised with the predicted channel set
-  // while the other CTAs arrive
-  if (SPEC)
-    for (int c = 0; c < min(nchunks, a.n_res); ++c) quant_chunk(c, pmk, true);
+  if (tid == 0) grid_arrive(a.ctl);
   K4TRACE(3);
-  if (tid == 0) k4_grid_wait(a.ctl, bar_base + n_bar * C);
+  if (tid == 0) grid_wait(a.ctl, bar_base + n_bar * C);
   __syncthreads();
   K4TRACE(13);
 
   // ---- C: statistics, redundantly in every CTA ------------------------------
   int big = 0, nonfinite = 0;
-  for (int c = tid; c < cols; c += kK4T) {
-    double v = __ldcg(sacc + c);
-    if (v < 0x1p-25) v = 0.0;  // all-zero column: only the 2^-127 terms of its zeros
-    big |= (v >= kK4Exact) && (v <= 65504.0 * static_cast<double>(rows));
+#pragma unroll 1
+  for (int c = tid; c < cols; c += kOT) {
+    const double v = __ldcg(sacc + c);
+    big |= (v >= kOExact) && (v <= 65504.0 * static_cast<double>(rows));
     nonfinite |= !(v < 0x1p100);  // an f16 inf / NaN element entered the sum as >= 2^128
     S[c] = v;
   }
   // the other accumulator buffer is the next call's: zero it (this call never reads it)
-  for (int64_t c = static_cast<int64_t>(b) * kK4T + tid; c < cols; c += static_cast<int64_t>(C) * kK4T)
+  for (int64_t c = static_cast<int64_t>(b) * kOT + tid; c < cols; c += static_cast<int64_t>(C) * kOT)
     __stcg(sacc_next + c, 0.0);
-  big = __syncthreads_or(big);
-  nonfinite = __syncthreads_or(nonfinite);
+  {
+    const int both = __syncthreads_or(big | (nonfinite << 1));
+    big = both & 1;
+    nonfinite = both >> 1;
+  }
   if (b == 0 && tid == 0 && nonfinite) raise_err(a.err, ADC_ERR_NONFINITE);
   if (big) {
     // some finite total reached 2^29: numpy's row-order sums behind a second barrier
-    k4_numpy_order_sums<DT>(a.x, rows, cols, a.sseq);
+    numpy_order_sums<BF>(a.x, rows, cols, a.sseq);
     __threadfence();
-    __syncthreads();
     ++n_bar;
-    if (tid == 0) {
-      k4_grid_arrive(a.ctl);
-      k4_grid_wait(a.ctl, bar_base + n_bar * C);
-    }
-    __syncthreads();
-    for (int c = tid; c < cols; c += kK4T) S[c] = __ldcg(a.sseq + c);
+    cta_grid_sync(a.ctl, bar_base + n_bar * C);
+    for (int c = tid; c < cols; c += kOT) S[c] = __ldcg(a.sseq + c);
     __syncthreads();
   }
   if (b == 0 && tid == 0) {
@@ -647,187 +832,142 @@ __global__ void __launch_bounds__(kK4T, 1) outlier_k4(K4Args a) {
     a.ctl[3] = static_cast<uint32_t>(cols);
   }
   K4TRACE(4);
-  const K4Tree &tr = a.tree;
-  // numpy pairwise sum of term(c) = S[c] or (S[c] - mean)^2; all threads call,
-  // all receive 0.0 + sum.  Leaves by 8-lane groups, internal nodes by warp 0.
-  auto tree_sum = [&](bool squared, double mean) -> double {
-    const int j8 = tid & 7;
-    constexpr int ng = kK4T / 8;
-    const int passes = (tr.n_leaves + ng - 1) / ng;
-    auto term = [&](int c) {
-      const double v = S[c];
-      if (!squared) return v;
-      const double d = __dsub_rn(v, mean);
-      return __dmul_rn(d, d);
-    };
-    for (int pass = 0; pass < passes; ++pass) {
-      const int g = (tid >> 3) + pass * ng;
-      const bool valid = g < tr.n_leaves;
-      const int lo = valid ? tr.leaf_lo[g] : 0, m = valid ? tr.leaf_n[g] : 0;
-      const int stop = m - (m % 8);
-      double r = 0.0;
-      if (valid && m >= 8) {
-        double v[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) v[i] = 8 * i < stop ? term(lo + 8 * i + j8) : 0.0;
-        r = v[0];
-#pragma unroll
-        for (int i = 1; i < 16; ++i)
-          if (8 * i < stop) r = __dadd_rn(r, v[i]);
-      }
-      const double x1 = __dadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1, 8));
-      const double x2 = __dadd_rn(x1, __shfl_down_sync(0xffffffffu, x1, 2, 8));
-      double x3 = __dadd_rn(x2, __shfl_down_sync(0xffffffffu, x2, 4, 8));
-      if (valid && j8 == 0) {
-        if (m < 8) x3 = 0.0;
-        for (int i = stop; i < m; ++i) x3 = __dadd_rn(x3, term(lo + i));
-        s_tv[g] = x3;
-      }
-    }
-    __syncthreads();
-    if (wid == 0) {
-      const int nl = tr.n_leaves;
-      int beg = 0;
-      for (int h = 0; h < tr.n_levels; ++h) {
-        const int end = tr.level_end[h];
-        for (int q = beg + lane; q < end; q += 32) s_tv[nl + q] = __dadd_rn(s_tv[tr.left[q]], s_tv[tr.right[q]]);
-        __syncwarp();
-        beg = end;
-      }
-      if (lane == 0) s_stat[3] = __dadd_rn(0.0, s_tv[beg == 0 ? 0 : nl + beg - 1]);
-    }
-    __syncthreads();
-    return s_stat[3];
-  };
   // 1) mean: any-order total (exact below 2^29), else the tree
   double part = 0.0;
-  for (int c = tid; c < cols; c += kK4T) part = __dadd_rn(part, S[c]);
+#pragma unroll 1
+  for (int c = tid; c < cols; c += kOT) part = __dadd_rn(part, S[c]);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part = __dadd_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
   if (lane == 0) s_red[wid] = part;
   __syncthreads();
-  double total = lane < kK4Warps ? s_red[lane] : 0.0;
+  double total = lane < kOW ? s_red[lane] : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) total = __dadd_rn(total, __shfl_xor_sync(0xffffffffu, total, o));
-  if (!(total < kK4Exact)) total = tree_sum(false, 0.0);
+  if (!(total < kOExact)) total = tree_sum(s_tree, S, false, 0.0, s_tv, &s_stat);
   const double mean = __ddiv_rn(__dadd_rn(0.0, total), static_cast<double>(cols));
   K4TRACE(10);
   // 2) population variance through the tree
-  const double var = __ddiv_rn(tree_sum(true, mean), static_cast<double>(cols));
+  const double var = __ddiv_rn(tree_sum(s_tree, S, true, mean, s_tv, &s_stat), static_cast<double>(cols));
   K4TRACE(11);
   const double sigma = __dsqrt_rn(var);
-  const double rsig = sigma != 0.0 ? __drcp_rn(sigma) : 0.0;
   K4TRACE(5);
+
   // 3) flags of a contiguous run of columns per thread, ranks by block scan
+  int rank_t0;  // flagged columns before the strip (rank of its first flagged column)
+  int nt;       // flagged columns in the strip
   {
-    const int run = static_cast<int>((cols + kK4T - 1) / kK4T);  // <= 32
+    const int run = static_cast<int>((cols + kOT - 1) / kOT);  // <= 32
     const int c0 = static_cast<int>(min(cols, static_cast<int64_t>(run) * tid));
     const int c1 = static_cast<int>(min(cols, static_cast<int64_t>(c0 + run)));
     uint32_t fb = 0;
-    for (int c = c0; c < c1; ++c) {
-      const double v = S[c];
-      const double qa = __dmul_rn(__dsub_rn(v, mean), rsig);
-      const double margin = __dadd_rn(__dmul_rn(fabs(qa), 0x1p-46), 0x1p-1000);
-      bool f = qa > __dadd_rn(a.thr, margin);
-      if (!f && !(qa < __dsub_rn(a.thr, margin))) f = __ddiv_rn(__dsub_rn(v, mean), sigma) > a.thr;
-      fb |= (f && sigma != 0.0 ? 1u : 0u) << (c - c0);
+    if (sigma != 0.0) {
+      // z = (s - mean) / sigma (numpy); q = (s - mean) * (1 / sigma) is within
+      // 2^-50 relative of z, so it decides every column outside a 2^-46
+      // relative margin around thr; inside it, the correctly rounded division
+      const double rsig = __drcp_rn(sigma);
+      const double hi = __dmul_rn(a.thr, 1.0 + 0x1p-46), lo = __dmul_rn(a.thr, 1.0 - 0x1p-46);
+#pragma unroll 1
+      for (int c = c0; c < c1; ++c) {
+        const double d = __dsub_rn(S[c], mean);
+        const double q = __dmul_rn(d, rsig);
+        bool f = q > fmax(hi, lo) + 0x1p-1000;
+        if (!f && q >= fmin(hi, lo) - 0x1p-1000) f = __ddiv_rn(d, sigma) > a.thr;
+        fb |= (f ? 1u : 0u) << (c - c0);
+      }
     }
     const int mine = __popc(fb);
+    // flagged columns of this run before the strip's first / past its last column
+    auto before_col = [&](int col) {
+      return col <= c0 ? 0 : col >= c1 ? mine : __popc(fb & ((1u << (col - c0)) - 1u));
+    };
+    int lt0 = before_col(tc0), lt1 = before_col(tc0 + W);
     int incl = mine;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += u;
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+      lt0 += __shfl_xor_sync(0xffffffffu, lt0, o);
+      lt1 += __shfl_xor_sync(0xffffffffu, lt1, o);
     }
-    if (lane == 31) s_int[wid] = incl;
-    __syncthreads();
-    int before = 0, total_k = 0;
-#pragma unroll
-    for (int w = 0; w < kK4Warps; ++w) {
-      const int cw = s_int[w];
-      before += w < wid ? cw : 0;
-      total_k += cw;
+    if (lane == 31) s_cnt[wid] = incl;
+    if (lane == 0) {
+      s_lt[wid] = lt0;
+      s_lt1[wid] = lt1;
     }
-    int pos = before + incl - mine;
+#pragma unroll 1
     for (int c = c0; c < c1; ++c) s_flag[c] = static_cast<uint8_t>((fb >> (c - c0)) & 1u);
-    for (uint32_t m = fb; m; m &= m - 1, ++pos) {
-      const int q = __ffs(m) - 1;
-      if (2 * static_cast<int64_t>(pos) <= cols) s_idx[pos] = static_cast<uint32_t>(c0 + q);
-      if (b == 0 && pos < a.k_cap && a.idx) a.idx[pos] = static_cast<uint32_t>(c0 + q);
+    __syncthreads();
+    K4TRACE(19);
+    int before = 0, total_k = 0, rank_t1 = 0;
+    rank_t0 = 0;
+#pragma unroll
+    for (int w2 = 0; w2 < kOW; ++w2) {
+      const int cw = s_cnt[w2];
+      before += w2 < wid ? cw : 0;
+      total_k += cw;
+      rank_t0 += s_lt[w2];
+      rank_t1 += s_lt1[w2];
     }
-    if (tid == 0) s_int[64] = total_k;
+    nt = rank_t1 - rank_t0;
+    int pos = before + incl - mine;
+    for (uint32_t m = fb; m; m &= m - 1, ++pos) {
+      const int q = c0 + __ffs(m) - 1;
+      if (b == 0 && a.idx && pos < a.k_cap) a.idx[pos] = static_cast<uint32_t>(q);
+      if (q >= tc0 && q < tc0 + W) s_tcol[pos - rank_t0] = static_cast<uint16_t>(q);
+    }
     if (b == 0 && tid == 0) {
       if (a.k_out) *a.k_out = total_k;
       if (2 * static_cast<int64_t>(total_k) > cols) raise_err(a.err, ADC_ERR_TOO_MANY_OUTLIERS);
       if (total_k > a.k_cap) raise_err(a.err, ADC_ERR_K_CAP);
     }
-    __syncthreads();
   }
-  const int k = s_int[64];
+  K4TRACE(20);
   // the new prediction (every CTA read the old one before its arrival)
-  if (SPEC && b == 0)
-    for (int c = tid; c < cols; c += kK4T) a.pflag[c] = s_flag[c];
+  if (b == 0)
+    for (int c = tid; c < cols; c += kOT) a.pflag[c] = s_flag[c];
+  __syncthreads();
   K4TRACE(6);
 
-  // ---- D: quantisation with the actual channel set --------------------------
+  // ---- D: re-quantise the groups whose channel set differs from the prediction
   {
-    uint32_t amk[16];
-    if (qon) {
-      k4_masks32(s_flag + 32 * qd, amk);
-      k4_rotate_masks(amk, rot);
-    } else {
+    uint32_t amk[8];
+    uint32_t dif = 0;
+    if (on) {
+      masks16(s_flag + tc0 + 16 * u, U.sw, amk);
 #pragma unroll
-      for (int i = 0; i < 16; ++i) amk[i] = 0u;
+      for (int i = 0; i < 8; ++i) dif |= amk[i] ^ pmk[i];
     }
-    bool chg = true;
-    if (SPEC) {
-      uint32_t dif = 0;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) dif |= amk[i] ^ pmk[i];
-      chg = qon && dif != 0u;
-    }
-    // a group is redone when any of its L4 lanes changed (groups never
-    // straddle rows: Q % L4 == 0, so a group's lanes share p2)
-    const uint32_t bal = __ballot_sync(0xffffffffu, chg);
-    const uint32_t gm = (L4 >= 32) ? 0xffffffffu : (((1u << L4) - 1u) << (lane & ~(L4 - 1)));
-    const bool redo = (bal & gm) != 0u;
-    if (__any_sync(0xffffffffu, redo))  // warp-uniform skip
-      for (int c = 0; c < nchunks; ++c) quant_chunk(c, amk, redo);
+    // a group is redone when any of its 8 lanes changed
+    const uint32_t bal = __ballot_sync(0xffffffffu, dif != 0u);
+    const bool redo = on && (bal & (0xffu << (lane & 24))) != 0u;
+    if (bal)
+      redo_rows<BF>(qo, a.x, cols, CR, a.slot_bytes, U, redo, make_uint4(amk[0], amk[1], amk[2], amk[3]),
+                    make_uint4(amk[4], amk[5], amk[6], amk[7]), slots, resident, r0, nrows, W, p, P, u, tc0);
   }
   K4TRACE(7);
 
-  // ---- E: side buffer: val[rank][r] = f16(x[r, idx[rank]]) for the slab ----
-  {
-    const int64_t ke = min(min(static_cast<int64_t>(k), a.k_cap), cols / 2);
-    if (a.val && ke > 0 && nrows > 0) {
-      const int items = static_cast<int>(ke) * nrows;
-      for (int it = tid; it < items; it += kK4T) {
-        const int rank = it / nrows, rr = it - rank * nrows;
-        const int cc = static_cast<int>(s_idx[rank]);
-        const int ch = rr / CR;
-        const unsigned char *src =
-            ch < a.n_res ? slots + ch * a.slot_bytes + (rr - ch * CR) * row_bytes + cc * EB
-                         : static_cast<const unsigned char *>(a.x) + ((r0 + rr) * cols + cc) * EB;
-        const uint16_t v = k4_one<DT>(src);
-        if ((v & 0x7fffu) >= 0x7c00u) raise_err(a.err, ADC_ERR_NONFINITE);  // bf16 beyond the f16 range
-        a.val[static_cast<int64_t>(rank) * rows + r0 + rr] = v;
-      }
-    }
-    if (k > ke && nrows > 0) k4_check_ungathered<DT>(a.x, cols, r0, nrows, s_flag, ke, k, a.err);
-  }
+  // ---- E: side buffer: val[rank][r] = f16(x[r, idx[rank]]) for the tile,
+  // unless the prediction held for every column (then A already wrote it)
+  int miss = 0;
+#pragma unroll 1
+  for (int c = tid; c < cols; c += kOT) miss |= s_flag[c] != s_pred[c];
+  miss = __syncthreads_or(miss);
+  if (miss && a.val && nt > 0 && nrows > 0)
+    side_buffer<BF>(a.x, rows, cols, CR, a.slot_bytes, a.k_cap, a.val, a.err, slots, resident, r0, nrows, W, tc0,
+                    s_tcol, nt, rank_t0);
   K4TRACE(8);
-  if (a.trace && lane == 0 && b < kK4TraceCtas) {
+  if (a.trace && lane == 0 && b < kOTraceCtas) {
     unsigned long long gt;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
-    if (tid == 0) g_k4trace[b * kK4TraceSlots + 12] = gt;
-    g_k4trace[b * kK4TraceSlots + 48 + wid] = gt;
+    if (tid == 0) g_k4trace[b * kOTraceSlots + 12] = gt;
+    g_k4trace[b * kOTraceSlots + 48 + wid] = gt;
   }
 }
 
 // ---------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------
-static int k4_optin_smem() {
+static int optin_smem() {
   static int v = 0;
   if (!v) {
     int dev = 0, s = 0;
@@ -840,13 +980,21 @@ static int k4_optin_smem() {
 }
 
 static std::atomic<int> g_k4_trace{0};
-static std::atomic<int> g_k4_mode{-1};  // 0: off (two launches), 1: single pass, 2: single pass + SPEC
+static std::atomic<int> g_k4_dbg{0};
+void set_k4_dbg(int v) { g_k4_dbg.store(v, std::memory_order_relaxed); }
+// 0: two launches, 1: single pass wherever eligible, 2: automatic (default):
+// the single pass where it measured faster -- tall tensors of <= 1024
+// columns (one strip), >= 2^25 elements ([131072,1024] bf16: 116 vs 138 us);
+// at [8192,1024] / [8192,4096] the two launches win (18.0 vs 22.3 us, 44.8 vs
+// 47.5 us: the one-wave cooperative launch, the serial statistics tail and
+// the per-row 2-byte work cost more than the L2 re-read they save).
+static std::atomic<int> g_k4_mode{-1};
 
 int k4_mode() {
   int v = g_k4_mode.load(std::memory_order_relaxed);
   if (v < 0) {
     const char *e = getenv("ADC_OUTLIER_PATH");
-    v = e ? (e[0] == '1' ? 1 : e[0] == 's' ? 2 : 0) : 0;  // default: two launches (measured faster, r2)
+    v = !e ? 2 : e[0] == '0' ? 0 : e[0] == '1' ? 1 : 2;
     g_k4_mode.store(v, std::memory_order_relaxed);
   }
   return v;
@@ -854,13 +1002,13 @@ int k4_mode() {
 void set_k4_mode(int v) { g_k4_mode.store(v, std::memory_order_relaxed); }
 void set_k4_trace(int v) { g_k4_trace.store(v, std::memory_order_relaxed); }
 int read_k4_trace(unsigned long long *host, int n) {
-  if (n > kK4TraceCtas * kK4TraceSlots) n = kK4TraceCtas * kK4TraceSlots;
+  if (n > kOTraceCtas * kOTraceSlots) n = kOTraceCtas * kOTraceSlots;
   return cudaMemcpyFromSymbol(host, g_k4trace, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
 }
 
-template <int DT, int L4, int J, bool SPEC>
-static int k4_go(const Ctx &c, const K4Args &a, size_t smem, int grid) {
-  auto kern = outlier_k4<DT, L4, J, SPEC>;
+template <bool BF>
+static int onepass_go(const Ctx &c, const OArgs &a, size_t smem, int grid) {
+  auto kern = outlier_onepass<BF>;
   static size_t configured = 0;  // per instantiation
   if (smem > configured) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)) != cudaSuccess) {
@@ -871,15 +1019,14 @@ static int k4_go(const Ctx &c, const K4Args &a, size_t smem, int grid) {
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(grid));
-  cfg.blockDim = dim3(kK4T);
+  cfg.blockDim = dim3(kOT);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = c.stream;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeCooperative;  // co-residency of the grid barrier
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
-  static const int coop = [] { const char *e = getenv("ADC_K4_NOCOOP"); return (e && e[0] == '1') ? 0 : 1; }();
-  cfg.numAttrs = coop;
+  cfg.numAttrs = 1;
   if (cudaLaunchKernelEx(&cfg, kern, a) != cudaSuccess) {
     cudaGetLastError();
     return 0;
@@ -895,105 +1042,70 @@ int launch_outlier_k4(const Ctx &c, const void *x, int dt, int64_t rows, int64_t
   const int mode = k4_mode();
   if (mode == 0) return 0;
   const int64_t n = rows * cols;
-  if (g != 32 && g != 64 && g != 128 && g != 256) return 0;
-  if (cols % g || cols % 32 || cols > 16384 || n >= (1ll << 31)) return 0;
-  const int L4 = static_cast<int>(g / 32);
+  if (mode == 2 && (cols > kOStripCols || n < (1ll << 25))) return 0;
+  if (g != 128 || cols % 128 || cols > 16384 || n >= (1ll << 31)) return 0;
+  if (dt != ADC_BF16 && dt != ADC_F16) return 0;
   if (reinterpret_cast<uintptr_t>(x) % 16 || reinterpret_cast<uintptr_t>(codes) % 16) return 0;
   if (k_cap > 0 && (!idx || !val)) return 0;
-  if (dt != ADC_BF16 && dt != ADC_F16 && dt != ADC_F32) return 0;
-  K4Args a{};
-  a.x = x;
+  OArgs a{};
+  a.x = static_cast<const uint16_t *>(x);
   a.rows = rows;
   a.cols = cols;
-  a.ucols = static_cast<int>(cols / 8);
-  int J = 1;
-  if (a.ucols <= kK4T) {
-    a.P = 1;
-    while (2 * a.P <= 32 && 2 * a.P * a.ucols <= kK4T) a.P *= 2;  // a power of two (xor-shuffle fold)
-  } else {
-    J = (a.ucols + kK4T - 1) / kK4T;
-    a.P = 1;
-    if (J > 4) return 0;
-  }
-  a.Q = static_cast<int>(cols / 32);
-  a.P2 = kK4T / a.Q;
   {
     static thread_local int tree_cols = -1;
-    static thread_local K4Tree tree;
+    static thread_local OTree tree;
     if (tree_cols != static_cast<int>(cols)) {
-      if (!build_k4_tree(static_cast<int>(cols), tree)) return 0;
+      if (!build_tree(static_cast<int>(cols), tree)) return 0;
       tree_cols = static_cast<int>(cols);
     }
     a.tree = tree;
   }
-  const int eb = dt == ADC_F32 ? 4 : 2;
-  const int64_t row_bytes = cols * eb;
-  const int grid = static_cast<int>(std::min<int64_t>(c.num_sms, rows));
-  const int64_t slab = (rows + grid - 1) / grid;
-  const size_t other = static_cast<size_t>(cols) * 8 + static_cast<size_t>((cols + 16 + 15) & ~15ll) +
-                       static_cast<size_t>((cols / 2 + 1) * 4 + 15) / 16 * 16;
-  const int static_smem = 4096;  // mbarriers, reductions, tree values (conservative)
-  const int64_t budget = k4_optin_smem() - static_smem - static_cast<int64_t>(other);
-  // chunks of ~16 KB of whole rows
-  int64_t cr = std::max<int64_t>(1, 16384 / row_bytes);
-  cr = std::min(cr, slab);
-  const int64_t slot_bytes = (cr * row_bytes + 127) / 128 * 128;
-  if (slot_bytes >= (1 << 20)) return 0;  // mbarrier tx-count limit
-  const int64_t nchunks = (slab + cr - 1) / cr;
-  const int64_t max_slots = std::min<int64_t>(kK4MaxSlots, budget / slot_bytes);
-  if (max_slots < 1) return 0;
-  if (nchunks <= max_slots) {
-    a.n_res = static_cast<int>(nchunks);
-    a.n_ring = 0;
+  const int G = static_cast<int>(cols / 128);
+  a.strips = (G + kOStripCols / 128 - 1) / (kOStripCols / 128);
+  a.slabs = static_cast<int>(std::min<int64_t>(c.num_sms / a.strips, rows));
+  if (a.slabs < 1) return 0;
+  a.rbase = static_cast<int>(rows / a.slabs);
+  a.rrem = static_cast<int>(rows % a.slabs);
+  const int grid = a.strips * a.slabs;
+  const int wmax = 128 * ((G + a.strips - 1) / a.strips);
+  // chunk = P_min rows of the widest strip (each row lane one row per chunk), 16 KB
+  a.chunk_rows = std::max(1, 16384 / wmax);  // 32 KB: two rows per row lane of the widest strip
+  a.slot_bytes = a.chunk_rows * wmax * 2;
+  const int64_t slab_rows = a.rbase + (a.rrem ? 1 : 0);
+  const int64_t nchunks = (slab_rows + a.chunk_rows - 1) / a.chunk_rows;
+  const int static_smem = 8192;  // mbarriers, tree values, strip column list (conservative)
+  const int64_t budget = optin_smem() - static_smem;
+  // statistics area: S[cols] doubles + flags; during B it stages P * W + W fold doubles
+  const int p_max = kOT / (wmax / 16);
+  const int64_t stats = std::max<int64_t>(cols * 8 + cols + 16,
+                                          (static_cast<int64_t>(p_max) * (wmax / 16) * 17 + wmax) * 8);
+  const int64_t stats_al = (stats + 127) / 128 * 128;
+  const int64_t pred_al = (cols + 16 + 127) / 128 * 128;
+  if (nchunks * a.slot_bytes + stats_al + pred_al <= budget && nchunks <= kOMaxSlots) {
+    a.n_slots = static_cast<int>(nchunks);
+    a.stats_off = static_cast<int>(nchunks * a.slot_bytes);
   } else {
-    if (max_slots < 3) return 0;
-    a.n_ring = static_cast<int>(std::min<int64_t>(4, max_slots - 1));
-    a.n_res = static_cast<int>(max_slots - a.n_ring);
+    a.n_slots = static_cast<int>(std::min<int64_t>(kOMaxSlots, (budget - pred_al) / a.slot_bytes));
+    a.stats_off = 0;  // overlays the ring (free once A is done)
+    if (a.n_slots < 2 || stats_al + pred_al > budget) return 0;
   }
-  a.chunk_rows = static_cast<int>(cr);
-  a.slot_bytes = static_cast<int>(slot_bytes);
-  const int64_t streamed = a.n_ring ? (slab - static_cast<int64_t>(a.n_res) * cr) * row_bytes * grid : 0;
-  a.keep = (a.n_ring && streamed <= (48ll << 20)) ? 1 : 0;
+  a.pred_off = static_cast<int>(std::max<int64_t>(a.stats_off + stats_al, static_cast<int64_t>(a.n_slots) * a.slot_bytes));
+  const size_t smem = static_cast<size_t>(a.pred_off + pred_al);
   a.thr = thr;
   a.k_cap = std::max<int64_t>(k_cap, 0);
   a.sacc = ws.k4acc;
   a.sseq = ws.colsum;
   a.ctl = ws.counters + 4;
   a.pflag = ws.pflag;
-  a.codes = reinterpret_cast<uint32_t *>(codes);
+  a.codes = codes;
   a.scales = scales;
   a.idx = idx;
   a.val = val;
   a.k_out = k_out;
   a.err = err;
   a.trace = g_k4_trace.load(std::memory_order_relaxed);
-  const size_t smem = static_cast<size_t>(a.n_res + a.n_ring) * slot_bytes + other;
-  const bool spec = mode == 2;
-#define ADC_K4_J(DTV, LV)                                                                      \
-  do {                                                                                         \
-    switch (J) {                                                                               \
-      case 1: return spec ? k4_go<DTV, LV, 1, true>(c, a, smem, grid) : k4_go<DTV, LV, 1, false>(c, a, smem, grid); \
-      case 2: return spec ? k4_go<DTV, LV, 2, true>(c, a, smem, grid) : k4_go<DTV, LV, 2, false>(c, a, smem, grid); \
-      case 3:                                                                                  \
-      case 4: return spec ? k4_go<DTV, LV, 4, true>(c, a, smem, grid) : k4_go<DTV, LV, 4, false>(c, a, smem, grid); \
-    }                                                                                          \
-    return 0;                                                                                  \
-  } while (0)
-#define ADC_K4_L(DTV)               \
-  switch (L4) {                     \
-    case 1: ADC_K4_J(DTV, 1);       \
-    case 2: ADC_K4_J(DTV, 2);       \
-    case 4: ADC_K4_J(DTV, 4);       \
-    case 8: ADC_K4_J(DTV, 8);       \
-  }
-  switch (dt) {
-    case ADC_BF16: ADC_K4_L(ADC_BF16); break;
-    case ADC_F16: ADC_K4_L(ADC_F16); break;
-    case ADC_F32: ADC_K4_L(ADC_F32); break;
-  }
-#undef ADC_K4_L
-#undef ADC_K4_J
-  return 0;
+  a.dbg = g_k4_dbg.load(std::memory_order_relaxed);
+  return dt == ADC_BF16 ? onepass_go<true>(c, a, smem, grid) : onepass_go<false>(c, a, smem, grid);
 }
 
 }  // namespace adc

@@ -61,8 +61,8 @@ struct Workspace {
   double *acc;           // cols       f64 atomic column-sum accumulators (zero at rest)
   double *k4acc;         // 2 x cols   single-pass kernel's bulk-reduction targets (double-buffered)
   uint32_t *macc;        // cols       u32 atomic column-max accumulators (zero at rest)
-  uint32_t *counters;    // 8          arrival counters ([0..3] colreduce / fused, [4..6] k4; zero at rest but [5])
-  uint8_t *pflag;        // cols + 8   previous outlier flags (fused kernel's prediction; any
+  uint32_t *counters;    // 8          arrival counters ([0..3] colreduce, [4..7] k4: barrier count / base / epoch / layout)
+  uint8_t *pflag;        // cols + 8   previous outlier flags (the single pass's prediction; any
                          //            content is valid, zero-fill = "no outliers")
   int32_t *node_lo;      // pairwise-tree nodes (used when cols > 16384)
   int32_t *node_n;
@@ -81,25 +81,11 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
 int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
                             const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
                             bool asym, void *y, int ot);
-// dequantise + flagged-channel overwrite in one launch (outputs within L2);
-// returns 1 when not eligible (then launch_group_decompress + launch_outlier_scatter)
-int launch_outlier_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
-                              const uint32_t *idx, const uint16_t *val, const int32_t *k_dev,
-                              int64_t k_cap, int64_t rows, int64_t cols, int64_t g, void *y, int ot);
-bool use_one_launch_outlier_decompress();
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot, const uint8_t *codes = nullptr,
                            const uint16_t *scales = nullptr, int64_t g = 0);
 
-// TMA-fed streaming variant of the fast group compress (stream.cu); L = lanes
-// per group at 8 elements per lane.
-int launch_group_compress_tma(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                              int L, bool asym, const uint8_t *zero_flag, uint8_t *codes,
-                              uint16_t *scales, uint16_t *offsets, uint32_t *err);
-// Tuning switch read once from the environment: ADC_COMPRESS_PATH=tma|regs (default regs).
-bool use_tma_compress();
-void set_compress_path(int v);
 bool use_epl32();
 void set_epl(int v);
 
@@ -107,17 +93,10 @@ int launch_outlier_gather(const Ctx &c, const void *x, int dt, const uint32_t *i
                           const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                           uint16_t *outl_val);
 
-// single-launch outlier-separated compress (fused.cu): returns 1 if it ran,
-// 0 if the shape / device is not eligible (the caller then uses the
-// colreduce + group_quant_fast pair, which writes identical bytes).
-int launch_outlier_fused(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols,
-                         int64_t g, double thr, int64_t k_cap, const Workspace &ws,
-                         uint8_t *codes, uint16_t *scales, uint32_t *idx, uint16_t *val,
-                         int32_t *k_out, uint32_t *err);
 // single-pass outlier-separated compress (k4.cu): returns 1 if it ran, 0 if
-// the shape is not eligible or the path is switched off (ADC_OUTLIER_PATH=2 /
-// adc_set_option("outlier_path", 0)); mode 2 (ADC_OUTLIER_PATH=s) speculates
-// with the previous call's channel set.
+// the shape is not eligible or not selected (ADC_OUTLIER_PATH /
+// adc_set_option("outlier_path", 0 two launches | 1 single pass | 2 auto)); the
+// caller then uses the colreduce + group_quant_fast pair (identical bytes).
 int launch_outlier_k4(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols, int64_t g,
                       double thr, int64_t k_cap, const Workspace &ws, uint8_t *codes,
                       uint16_t *scales, uint32_t *idx, uint16_t *val, int32_t *k_out,
@@ -125,25 +104,8 @@ int launch_outlier_k4(const Ctx &c, const void *x, int dt, int64_t rows, int64_t
 int k4_mode();
 void set_k4_mode(int v);
 void set_k4_trace(int v);
+void set_k4_dbg(int v);
 int read_k4_trace(unsigned long long *host, int n);
-// ADC_OUTLIER_PATH=2 selects the two-launch path (A/B testing).
-bool use_fused_outlier();
-void set_fused_outlier(int v);
-void set_fused_trace(int v);
-int read_fused_trace(unsigned long long *host, int n);
-
-// Speculative outlier-separated first pass (spec.cu): column sums AND the
-// symmetric quantisation with the previous call's channel set (ws.pflag) in
-// one read of x; the last CTA computes the statistics and writes *miss = 1
-// when the actual channel set differs (then the quantiser launch redoes the
-// codes).  Returns 0 if the shape is not eligible.
-int launch_outlier_spec(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols, int64_t g,
-                        double thr, int64_t k_cap, const Workspace &ws, uint8_t *codes,
-                        uint16_t *scales, uint32_t *idx, int32_t *k_out, uint32_t *err,
-                        uint32_t *miss);
-bool use_outlier_spec();
-void set_outlier_spec(int v);
-
 // int8 extension (int8.cu; parity unpinned, oracle/int8_oracle.py)
 int launch_int8_compress(const Ctx &c, const void *x, int dt, int64_t n, int64_t g, int8_t *codes,
                          float *scales, uint32_t *err);

@@ -361,177 +361,4 @@ int launch_colstats_max(const Ctx &c, const void *x, int dt, int64_t rows, int64
   return 0;
 }
 
-// ---------------------------------------------------------------------------
-// Speculative first pass of the outlier-separated compressor: the column
-// statistics of colreduce<SUM> AND the symmetric quantisation of every unit
-// with the PREDICTED channel set (the previous call's flags, ws.pflag) in the
-// same read of x.  A warp covers 32 consecutive 8-column units of one row
-// (a 256-column strip), so a group of 8L elements lies on L aligned lanes and
-// the group reductions are the quantiser's own shuffles; each thread's
-// columns are fixed, so the predicted zeroing is four constant AND masks.
-// The last CTA evaluates the statistics (identical to colreduce) and compares
-// the actual flags with the prediction: *miss = 0 lets the quantiser launch
-// that follows skip its work (it still gathers the side buffer); on a miss it
-// re-quantises everything and the prediction is updated.  Outlier channel
-// sets persist across training iterations (Fig. 4a), so in steady
-// state x is read from HBM once.
-template <int DT, int L>
-__global__ void __launch_bounds__(kThreads, 4)
-    colreduce_spec(const void *__restrict__ x, ColArgs a, uint32_t *__restrict__ codes,
-                   uint16_t *__restrict__ scales, uint8_t *__restrict__ pflag, uint32_t *__restrict__ miss) {
-  pdl_entry();
-  __shared__ __align__(16) unsigned char s_buf[kTailSmem];
-  double(*red)[32][8] = reinterpret_cast<double(*)[32][8]>(s_buf);
-  __shared__ int s_last;
-  constexpr bool BF = DT == ADC_BF16;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int64_t cols = a.cols, rows = a.rows;
-  const int64_t cu = static_cast<int64_t>(blockIdx.x) * 32 + tx;  // always < cols / 8 (cols % 256 == 0)
-  const int64_t units_row = cols / 8;
-  uint32_t mk[4] = {0xffffffffu, 0xffffffffu, 0xffffffffu, 0xffffffffu};
-  zero_apply8(mk, __ldg(reinterpret_cast<const uint2 *>(pflag + 8 * cu)));
-  const char *xb = static_cast<const char *>(x) + cu * 16;
-
-  double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  auto unit = [&](int64_t r, uint4 h) {
-    const uint32_t w[4] = {h.x, h.y, h.z, h.w};
-    const uint32_t hf[4] = {BF ? bf2_to_h2(w[0]) : w[0], BF ? bf2_to_h2(w[1]) : w[1],
-                            BF ? bf2_to_h2(w[2]) : w[2], BF ? bf2_to_h2(w[3]) : w[3]};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      acc[2 * j] = __dadd_rn(acc[2 * j], fabs(h_lo_f64(hf[j])));
-      acc[2 * j + 1] = __dadd_rn(acc[2 * j + 1], fabs(h_hi_f64(hf[j])));
-    }
-    const uint32_t wm[4] = {w[0] & mk[0], w[1] & mk[1], w[2] & mk[2], w[3] & mk[3]};
-    uint16_t sb;
-    bool bad;
-    const uint32_t code = sym_unit8<BF, L>(wm, true, sb, bad);
-    const int64_t u = r * units_row + cu;
-    codes[u] = code;
-    if ((tx & (L - 1)) == 0) {
-      scales[u / L] = sb;
-      if (bad) raise_err(a.err, ADC_ERR_NONFINITE);
-    }
-  };
-  const int64_t step = static_cast<int64_t>(gridDim.y) * kRowLanes;
-  int64_t r = static_cast<int64_t>(blockIdx.y) * kRowLanes + ty;
-  for (; r + step < rows; r += 2 * step) {  // 2 rows in flight (warp-uniform)
-    uint4 h[2];
-#pragma unroll
-    for (int q = 0; q < 2; ++q) h[q] = ld_keep16(xb + (r + q * step) * cols * 2);
-#pragma unroll
-    for (int q = 0; q < 2; ++q) unit(r + q * step, h[q]);
-  }
-  for (; r < rows; r += step) unit(r, ld_keep16(xb + r * cols * 2));
-
-#pragma unroll
-  for (int j = 0; j < 8; ++j) red[ty][tx][j] = acc[j];
-  __syncthreads();
-  {
-    const int t = threadIdx.x, ctx = t >> 3, cj = t & 7;
-    const int64_t c = static_cast<int64_t>(blockIdx.x) * kStripCols + t;
-    double v = red[0][ctx][cj];
-#pragma unroll
-    for (int q = 1; q < kRowLanes; ++q) v = __dadd_rn(v, red[q][ctx][cj]);
-    if (c < cols && v != 0.0) atomicAdd(a.acc + c, v);
-  }
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) s_last = atomicAdd(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const bool s_smem = cols <= kSmemSumCols;
-  double *s_S = reinterpret_cast<double *>(s_buf);
-  int big = 0;
-  for (int64_t c = threadIdx.x; c < cols; c += kThreads) {
-    const double v = __ldcg(a.acc + c);
-    __stcg(a.acc + c, 0.0);
-    __stcg(a.S + c, v);
-    if (s_smem) s_S[c] = v;
-    big |= !(v < kExactLimit);
-  }
-  if (threadIdx.x == 0) a.done_cnt[0] = 0;
-  big = __syncthreads_or(big);
-  if (big) {
-    numpy_order_sums<DT>(x, rows, cols, a.S);
-    __syncthreads();
-    if (s_smem)
-      for (int64_t c = threadIdx.x; c < cols; c += kThreads) s_S[c] = __ldcg(a.S + c);
-    __syncthreads();
-  }
-  if (s_smem)
-    outlier_stats_block<true>(s_S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out, a.err,
-                              true, s_buf + kSmemSumCols * 8);
-  else
-    outlier_stats_block<false>(a.S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out, a.err,
-                               true, s_buf);
-  // prediction check: every actual flag against the predicted one
-  int m = 0;
-  for (int64_t c = threadIdx.x; c < cols; c += kThreads) m |= (__ldcg(a.flag + c) != 0) != (pflag[c] != 0);
-  m = __syncthreads_or(m);
-  if (m)
-    for (int64_t c = threadIdx.x; c < cols; c += kThreads) pflag[c] = __ldcg(a.flag + c);
-  if (threadIdx.x == 0) *miss = m ? 1u : 0u;
-}
-
-static std::atomic<int> g_spec{-1};
-bool use_outlier_spec() {
-  int v = g_spec.load(std::memory_order_relaxed);
-  if (v < 0) {
-    // measured (B200, bf16, predictions hitting): 22.4 / 57.6 / 166 us vs
-    // 19.4 / 47.9 / 146 us for [8192,1024] / [8192,4096] / [131072,1024] with
-    // the plain two launches -- the combined pass runs at 1.9 TB/s (16 warps
-    // per SM, 85 M instructions for 268 MB) and the side-buffer gather left
-    // in the second launch is latency-bound -- so it is opt-in
-    const char *e = getenv("ADC_OUTLIER_SPEC");
-    v = (e && e[0] == '1') ? 1 : 0;
-    g_spec.store(v, std::memory_order_relaxed);
-  }
-  return v == 1;
-}
-void set_outlier_spec(int v) { g_spec.store(v ? 1 : 0, std::memory_order_relaxed); }
-
-int launch_outlier_spec(const Ctx &c, const void *x, int dt, int64_t rows, int64_t cols, int64_t g,
-                        double thr, int64_t k_cap, const Workspace &ws, uint8_t *codes,
-                        uint16_t *scales, uint32_t *idx, int32_t *k_out, uint32_t *err,
-                        uint32_t *miss) {
-  if (!use_outlier_spec()) return 0;
-  if (dt != ADC_BF16 && dt != ADC_F16) return 0;
-  if (cols % kStripCols || g % 8 || kStripCols % g || rows * cols >= (1ll << 31)) return 0;
-  if (!fast_cols(x, cols) || reinterpret_cast<uintptr_t>(codes) % 4) return 0;
-  const int L = static_cast<int>(g / 8);
-  ColArgs a = make_args(rows, cols, ws);
-  a.do_stats = 1;
-  a.too_many_check = 1;
-  a.thr = thr;
-  a.k_cap = k_cap;
-  a.idx = idx;
-  a.k_out = k_out;
-  a.err = err;
-  uint32_t *codes32 = reinterpret_cast<uint32_t *>(codes);
-#define ADC_SPEC_GO(DTV, LV)                                                                       \
-  {                                                                                                \
-    const dim3 grid = col_grid(c, colreduce_spec<DTV, LV>, rows, cols);                           \
-    launch_k(colreduce_spec<DTV, LV>, grid, dim3(kThreads), 0, c.stream, x, a, codes32, scales,    \
-             ws.pflag, miss);                                                                      \
-    note_launches(1);                                                                              \
-    return 1;                                                                                      \
-  }
-#define ADC_SPEC_L(DTV)          \
-  switch (L) {                   \
-    case 1: ADC_SPEC_GO(DTV, 1)  \
-    case 2: ADC_SPEC_GO(DTV, 2)  \
-    case 4: ADC_SPEC_GO(DTV, 4)  \
-    case 8: ADC_SPEC_GO(DTV, 8)  \
-    case 16: ADC_SPEC_GO(DTV, 16) \
-    case 32: ADC_SPEC_GO(DTV, 32) \
-    default: return 0;           \
-  }
-  if (dt == ADC_BF16) ADC_SPEC_L(ADC_BF16) else ADC_SPEC_L(ADC_F16)
-#undef ADC_SPEC_L
-#undef ADC_SPEC_GO
-  return 0;
-}
-
 }  // namespace adc

@@ -320,11 +320,11 @@ def test_graph_replay_matches_eager(torch_cuda, scheme, group):
     assert int(slot.status[0]) == 0
 
 
-K4_PATHS = {"two_launch": 0, "single_pass": 1, "single_pass_spec": 2}
+K4_PATHS = {"two_launch": 0, "single_pass": 1}
 
 
-def _k4_eligible(shape, group):
-    return group in (32, 64, 128, 256) and shape[1] % group == 0 and shape[1] % 32 == 0 and shape[1] <= 16384
+def _k4_eligible(shape, group, dtype_name):
+    return group == 128 and shape[1] % 128 == 0 and shape[1] <= 16384 and dtype_name in ("bfloat16", "float16")
 
 
 @pytest.mark.parametrize("path", sorted(K4_PATHS))
@@ -353,25 +353,26 @@ def test_outlier_paths_match_oracle(torch_cuda, shape, dtype_name, group, path):
         n0 = _lib.lib().adc_kernel_launches()
         ct = adc.compress(xt, spec)
         torch.cuda.synchronize()
-        if path != "two_launch" and _k4_eligible(shape, group):
+        if path != "two_launch" and _k4_eligible(shape, group, dtype_name):
             assert _lib.lib().adc_kernel_launches() - n0 == 1
         got = device_run(xt, cases.OUTL, group, 3.0)
     finally:
-        _lib.set_option("outlier_path", 0)
+        _lib.set_option("outlier_path", 2)
     assert cases.norm_digest(*got) == cases.norm_digest(*want)
     idx = want[0]["idx"]
     assert ct.outlier_count == (0 if idx is None else len(idx))
 
 
-@pytest.mark.parametrize("path", ["single_pass", "single_pass_spec"])
+@pytest.mark.parametrize("path", ["single_pass", "two_launch"])
 @pytest.mark.parametrize("dtype_name,cols,rows", [("bfloat16", 1024, 2048), ("float32", 768, 2048),
                                                   ("float16", 4096, 2048), ("bfloat16", 3072, 2048),
-                                                  ("bfloat16", 4096, 16384)])
+                                                  ("bfloat16", 4096, 16384), ("bfloat16", 11008, 4096),
+                                                  ("float16", 896, 777), ("bfloat16", 128, 5000)])
 def test_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, rows, path):
     """A slot's workspace carries the previous call's channel set (and the
-    double-buffered column accumulator); the speculative single pass
-    quantises with the predicted set and re-quantises the groups whose
-    channels changed.  Alternate inputs with different / equal outlier sets
+    double-buffered column accumulator); the single pass quantises with the
+    predicted set and re-quantises the groups whose channels changed
+    (resident tiles from shared memory, streamed tiles from global memory).  Alternate inputs with different / equal outlier sets
     through ONE slot and check every call against the oracle."""
     torch = torch_cuda
     import paper_2508_00806_b200 as adc
@@ -407,7 +408,7 @@ def test_outlier_prediction_hits_and_misses(torch_cuda, dtype_name, cols, rows, 
             np.testing.assert_array_equal(y.cpu().numpy().view(np.uint32), wdeq.view(np.uint32))
             assert int(slot.status[0]) == 0
     finally:
-        _lib.set_option("outlier_path", 0)
+        _lib.set_option("outlier_path", 2)
 
 
 @pytest.mark.parametrize("rows", [16384, 16384 + 256])
@@ -559,25 +560,3 @@ def test_concurrent_streams_are_reentrant(torch_cuda):
             for a, b in zip(snapshot(slot, y), want):
                 assert torch.equal(a.view(torch.uint8), b.view(torch.uint8))
             assert int(slot.status[0]) == 0
-
-
-@pytest.mark.parametrize("shape,dtype_name", [((8192, 1024), "bfloat16"), ((1000, 40), "float32"),
-                                              ((2048, 4096), "float16"), ((333, 1024), "bfloat16")])
-def test_one_launch_outlier_decompress(torch_cuda, shape, dtype_name, monkeypatch):
-    """The opt-in single-launch outlier decompress (ADC_OUTLIER_DEQ1=1) writes
-    the same bytes as dequantise + scatter."""
-    torch = torch_cuda
-    import paper_2508_00806_b200 as adc
-    rng = np.random.default_rng(shape[1])
-    x = rng.normal(size=shape).astype(np.float32)
-    hot = rng.choice(shape[1], max(2, shape[1] // 60), replace=False)
-    hot[1] = hot[0] ^ 1  # two flagged channels inside one 8-column unit
-    x[:, hot] *= 30
-    xt = torch.from_numpy(x).to(getattr(torch, dtype_name)).cuda()
-    ct = adc.compress(xt, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED))
-    for out in (torch.float32, torch.bfloat16):
-        monkeypatch.setenv("ADC_OUTLIER_DEQ1", "0")
-        want = adc.decompress(ct, out)
-        monkeypatch.setenv("ADC_OUTLIER_DEQ1", "1")
-        got = adc.decompress(ct, out)
-        assert torch.equal(got.view(torch.uint8), want.view(torch.uint8))

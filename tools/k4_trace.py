@@ -20,10 +20,12 @@ import paper_2508_00806_b200 as adc  # noqa: E402
 from paper_2508_00806_b200 import _lib  # noqa: E402
 from paper_2508_00806_b200.slots import CodecSlot  # noqa: E402
 
-PHASES = [(9, "setup"), (1, "A: stream + column sums"), (2, "B: fold"), (3, "B: reduce + arrive (+spec quant)"),
-          (13, "B: barrier wait"),
-          (4, "C: load sums"), (10, "C: mean"), (11, "C: variance tree"), (5, "C: sqrt / rcp"),
-          (6, "C: flags + ranks"), (7, "D: quantise"), (8, "E: side buffer")]
+PHASES = [(14, "setup: mbarrier init"), (15, "setup: chunk issue (warp 0)"), (18, "setup: prediction scan"),
+          (16, "setup: prediction masks"), (9, "setup: nibble masks"), (1, "A: sums + quantise (warp 0)"),
+          (17, "A: all warps done"), (2, "B: fold"), (3, "B: reduce + arrive"), (13, "B: barrier wait"),
+          (4, "C: load sums"), (10, "C: mean"), (11, "C: variance tree"), (5, "C: sqrt"),
+          (19, "C: flags + scan"), (20, "C: idx / k"), (6, "C: tile list + prediction"),
+          (7, "D: re-quantise"), (8, "E: side buffer")]
 
 
 def graph_time(fns, reps=20):
@@ -99,7 +101,7 @@ def main():
                   f" | phase med {statistics.median(dur) / mhz:6.2f} max {max(dur) / mhz:6.2f} us")
             prev = ends
         # eager single calls with a sync between (launch gaps excluded by events around each)
-        for mode in (0, 1):
+        for mode in (0, 1):  # 0: two launches, 1: single pass
             _lib.set_option("outlier_path", mode)
             ts = []
             for it in range(10):
@@ -112,10 +114,24 @@ def main():
                 ts.append(e0.elapsed_time(e1) * 1e3)
             print(f"  eager mode {mode}: per call {sorted(ts)[len(ts) // 2]:.1f} us (median of 10)")
         slots = [CodecSlot(rows, cols, spec, dtype, dtype, k_cap=cols // 8) for _ in range(min(nbuf, 4))]
-        k = None
-        for mode, name in ((0, "two launches"), (1, "single pass"), (2, "single pass + spec")):
+        # a second input family with another outlier channel set: alternating the
+        # two through one slot makes every call mispredict
+        alt = []
+        for i in range(len(slots)):
+            x = torch.randn(rows, cols, device="cuda").to(dtype)
+            x[:, 5::89] *= 30
+            alt.append(x)
+        for mode, name, srcs in ((0, "two launches", None), (1, "single pass (hit)", None),
+                                 (1, "single pass (miss)", alt)):
             _lib.set_option("outlier_path", mode)
-            t = graph_time([lambda sp, sl=sl, x=x: sl.compress_ptr(x.data_ptr(), sp) for sl, x in zip(slots, xs)])
+            fns = []
+            for j, (sl, x) in enumerate(zip(slots, xs)):
+                fns.append(lambda sp, sl=sl, x=x: sl.compress_ptr(x.data_ptr(), sp))
+                if srcs is not None:
+                    fns.append(lambda sp, sl=sl, x=srcs[j]: sl.compress_ptr(x.data_ptr(), sp))
+            if srcs is not None:  # interleave: slot j gets xs[j], alt[j], xs[j], ...
+                fns = fns * 2
+            t = graph_time(fns)
             kk = int(slots[0].k_status[1])
             bc, _ = slots[0].algorithmic_bytes(kk)
             print(f"  {name:20s} {t:7.1f} us  {bc / t / 1e3:6.0f} GB/s  (k={kk})")
