@@ -54,7 +54,7 @@ def timeit(fns):
 
 
 def main():
-    shapes = [(8192, 1024), (8192, 4096), (8192, 3072), (131072, 1024)]
+    shapes = [(8192, 1024), (8192, 4096), (8192, 3072), (131072, 1024), (131072, 64)]
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     if len(args) == 2:
         shapes = [(int(args[0]), int(args[1]))]
