@@ -199,6 +199,22 @@ ADC_API int adc_decompress_int8(const int8_t *codes, const float *scales, int64_
                                 int64_t group_size, void *y, int out_dtype, void *stream);
 
 /*
+ * EXTENSION, no reference counterpart (north_star "fp32-scale storage
+ * option"; the reference rounds every scale to float16, codec.py:192-196):
+ * the symmetric group int4 codec with FLOAT32 scales.  Parity unpinned,
+ * restated in oracle/int8_oracle.py: h = f16(x); s = f32(max|h| / 8) per
+ * group of group_size row-major elements; code = clip(rint_even(f32(h / s')),
+ * -8, 7) (s' = 1 for an all-zero group), nibbles packed as the reference's
+ * (codec.py:199-203); decompress = f32(code * s) (then RNE to the output
+ * dtype).  codes: ceil(rows*cols/2) bytes; scales: ceil(rows*cols/group) f32.
+ */
+ADC_API int adc_compress_int4f32(const void *x, int in_dtype, int64_t rows, int64_t cols,
+                                 int64_t group_size, uint8_t *codes, float *scales, uint32_t *err_word,
+                                 void *stream);
+ADC_API int adc_decompress_int4f32(const uint8_t *codes, const float *scales, int64_t rows, int64_t cols,
+                                   int64_t group_size, void *y, int out_dtype, void *stream);
+
+/*
  * Device-side ADC1 wire format; replaces serialize (codec.py:432-459) without
  * a host round trip: writes the 25-byte header, metadata, codes and outlier
  * side buffer of a compressed tensor (the device buffers adc_compress wrote)

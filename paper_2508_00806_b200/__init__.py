@@ -14,6 +14,7 @@ from .codec import (
     SERIALIZED_HEADER_BYTES,
     CodecReport,
     CompressedTensor,
+    Int4F32Tensor,
     Int8Tensor,
     Scheme,
     SchemeSpec,
@@ -24,6 +25,7 @@ from .codec import (
     decompress,
     decompress_into,
     dequantize,
+    dequantize_int4_f32,
     dequantize_int8,
     deserialize,
     detect_outlier_channels,
@@ -32,6 +34,7 @@ from .codec import (
     pack_bitmask,
     packed_payload_bytes,
     quantize_asymmetric,
+    quantize_int4_f32,
     quantize_int8,
     quantize_symmetric,
     scheme_for,

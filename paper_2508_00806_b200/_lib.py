@@ -49,6 +49,8 @@ SIGNATURES = {
                                  _i64, _vp, C.c_int, _vp]),
     "adc_compress_int8": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
     "adc_decompress_int8": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, C.c_int, _vp]),
+    "adc_compress_int4f32": (C.c_int, [_vp, C.c_int, _i64, _i64, _i64, _vp, _vp, _vp, _vp]),
+    "adc_decompress_int4f32": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, C.c_int, _vp]),
     "adc_serialize": (C.c_int, [C.c_int, _vp, _vp, _vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64, _vp, _sz,
                                 _vp, _vp, _vp]),
     "adc_parse_header": (C.c_int, [C.c_char_p, C.c_uint64, C.POINTER(WireHeader)]),

@@ -711,3 +711,53 @@ def dequantize_int8(ct: Int8Tensor, out_dtype: torch.dtype = torch.float32) -> t
                                         ct.group_size, y.data_ptr(), _DT[out_dtype], _stream())
     _lib.check(st, "decompress_int8")
     return y
+
+
+@dataclass
+class Int4F32Tensor:
+    """Symmetric group int4 codes with float32 scales (payload ceil(N/2) + 4*G bytes)."""
+    rows: int
+    cols: int
+    group_size: int
+    codes: torch.Tensor   # uint8 (ceil(rows*cols/2),), the reference nibble order
+    scales: torch.Tensor  # float32 (n_groups,)
+    status: torch.Tensor  # int32 [error word, unused]
+    shape: tuple = ()
+
+    @property
+    def compressed_size_bytes(self) -> int:
+        return self.codes.numel() + 4 * self.scales.numel()
+
+    @property
+    def compression_ratio(self) -> float:
+        return 2 * self.rows * self.cols / self.compressed_size_bytes
+
+
+def quantize_int4_f32(x, group_size: int = DEFAULT_GROUP_SIZE, *, check: bool = True) -> Int4F32Tensor:
+    """int4 / float32-scale extension compress (device); the reference's errors in check mode."""
+    if group_size < 1:
+        raise ValidationError(f"group_size must be positive, got {group_size}")
+    shape = tuple(x.shape) if hasattr(x, "shape") else ()
+    t = _as_device_matrix(x)
+    rows, cols = t.shape
+    n = rows * cols
+    dev = t.device
+    codes = torch.empty((n + 1) // 2, dtype=torch.uint8, device=dev)
+    scales = torch.empty((n + group_size - 1) // group_size, dtype=torch.float32, device=dev)
+    status = torch.zeros(2, dtype=torch.int32, device=dev)
+    st = _lib.lib().adc_compress_int4f32(t.data_ptr(), _DT[t.dtype], rows, cols, group_size, codes.data_ptr(),
+                                         scales.data_ptr(), status.data_ptr(), _stream())
+    _lib.check(st, "compress_int4f32")
+    ct = Int4F32Tensor(rows, cols, group_size, codes, scales, status, shape)
+    if check:
+        raise_for_error_word(int(status[0].item()) & 0xffffffff, rows=rows, cols=cols, k=0)
+    return ct
+
+
+def dequantize_int4_f32(ct: Int4F32Tensor, out_dtype: torch.dtype = torch.float32) -> torch.Tensor:
+    y = torch.empty((ct.rows, ct.cols), dtype=out_dtype, device=ct.codes.device)
+    st = _lib.lib().adc_decompress_int4f32(ct.codes.data_ptr(), ct.scales.data_ptr(), ct.rows, ct.cols,
+                                           ct.group_size, y.data_ptr(), _DT[out_dtype], _stream())
+    _lib.check(st, "decompress_int4f32")
+    return y
+

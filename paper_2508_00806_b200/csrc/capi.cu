@@ -286,6 +286,29 @@ int adc_decompress_int8(const int8_t *codes, const float *scales, int64_t rows, 
   return check_launch("int8_decompress");
 }
 
+int adc_compress_int4f32(const void *x, int in_dtype, int64_t rows, int64_t cols, int64_t group_size,
+                         uint8_t *codes, float *scales, uint32_t *err_word, void *stream) {
+  if (rows < 1 || cols < 1) return fail(ADC_EINVAL, "activation matrix must have at least one element");
+  if (!x || !codes || !scales) return fail(ADC_EINVAL, "null buffer");
+  if (!valid_float_dtype(in_dtype)) return fail(ADC_EINVAL, "activation dtype must be f32, bf16 or f16");
+  if (group_size < 1) return fail(ADC_EINVAL, "group_size must be positive");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  if (launch_int4f32_compress(c, x, in_dtype, rows * cols, group_size, codes, scales, err_word))
+    return fail(ADC_EINVAL, "int4/f32 dispatch");
+  return check_launch("int4f32_compress");
+}
+
+int adc_decompress_int4f32(const uint8_t *codes, const float *scales, int64_t rows, int64_t cols,
+                           int64_t group_size, void *y, int out_dtype, void *stream) {
+  if (rows < 1 || cols < 1 || !codes || !scales || !y) return fail(ADC_EINVAL, "bad arguments");
+  if (group_size < 1) return fail(ADC_EINVAL, "group_size must be positive");
+  if (!valid_float_dtype(out_dtype)) return fail(ADC_EINVAL, "output dtype must be f32, bf16 or f16");
+  Ctx c{static_cast<cudaStream_t>(stream), sm_count()};
+  if (launch_int4f32_decompress(c, codes, scales, rows * cols, group_size, y, out_dtype))
+    return fail(ADC_EINVAL, "int4/f32 decompress dispatch (codes need 4-byte, output 16-byte alignment)");
+  return check_launch("int4f32_decompress");
+}
+
 int adc_serialize(int scheme, const uint16_t *scales, const uint16_t *offsets, const uint8_t *codes,
                   const uint32_t *outlier_idx, const uint16_t *outlier_val, const int32_t *k_dev,
                   int64_t k_cap, int64_t rows, int64_t cols, int64_t group_size, uint8_t *out,

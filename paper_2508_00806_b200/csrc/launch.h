@@ -111,6 +111,10 @@ int launch_int8_compress(const Ctx &c, const void *x, int dt, int64_t n, int64_t
                          float *scales, uint32_t *err);
 int launch_int8_decompress(const Ctx &c, const int8_t *codes, const float *scales, int64_t n, int64_t g,
                            void *y, int ot);
+int launch_int4f32_compress(const Ctx &c, const void *x, int dt, int64_t n, int64_t g, uint8_t *codes,
+                            float *scales, uint32_t *err);
+int launch_int4f32_decompress(const Ctx &c, const uint8_t *codes, const float *scales, int64_t n, int64_t g,
+                              void *y, int ot);
 
 // device-side ADC1 serialisation (wire.cu)
 int launch_wire_serialize(const Ctx &c, int scheme, int64_t rows, int64_t cols, int64_t group,

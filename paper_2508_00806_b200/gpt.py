@@ -8,7 +8,7 @@ activations autograd saves, as operators with a LayerKind:
 
   1 block_input  linear        LN1 input (the block checkpoint; never recomputed)
   2 ln1_out      layer_norm    LN1 output, saved by the QKV projection
-  3 qkv          qkv_matrix    q, k, v in head layout [b, nh, s, hd] (per-channel over hd)
+  3 qkv          qkv_matrix    the fused QKV projection [b, s, 3h] (per-channel over 3h)
   4 attn_softmax softmax       softmax probabilities
   5 attn_mask    dropout_mask  attention-dropout keep mask (bool)
   6 attn_weights score         dropped probabilities, saved by probs @ v
@@ -103,46 +103,77 @@ class _Softmax(torch.autograd.Function):
         return p * (g - (g * p).sum(dim=-1, keepdim=True)), None
 
 
-class _Memo:
-    """Recompute recipe shared by several outputs of one operator (q, k, v):
-    the first unpack runs the operator, the others reuse its result."""
-
-    def __init__(self, fn):
-        self.fn = fn
-        self.key = None
-        self.out = None
-
-    def part(self, i):
-        def run(a):
-            if self.key is not a:
-                self.out, self.key = self.fn(a), a
-            return self.out[i]
-        return run
-
-
-def split_heads(qkv, n_head):
-    """[b, s, 3h] -> q, k, v as contiguous [b, nh, s, hd] (what the attention
-    matmuls consume without further copies)."""
+def head_parts(qkv, n_head):
+    """[b, s, 3h] -> q, k, v as strided [b, nh, s, hd] views (no copies)."""
     b, s, three_h = qkv.shape
     h = three_h // 3
     parts = qkv.view(b, s, 3, n_head, h // n_head).permute(2, 0, 3, 1, 4)
-    return parts[0].contiguous(), parts[1].contiguous(), parts[2].contiguous()
+    return parts[0], parts[1], parts[2]
 
 
-def _causal_scores(q, k, scale):
-    s = q.shape[-2]
-    scores = torch.matmul(q, k.transpose(-2, -1)) * scale
-    causal = torch.ones(s, s, dtype=torch.bool, device=q.device).triu_(1)
-    return scores.masked_fill(causal, float("-inf"))
+def _causal(s, device):
+    return torch.ones(s, s, dtype=torch.bool, device=device).triu_(1)
 
 
-def _causal_softmax(q, k, scale, tag=None):
-    return _Softmax.apply(_causal_scores(q, k, scale), tag)
+def _qkv_grad(qkv, n_head, dq=None, dk=None, dv=None):
+    """[b, s, 3h] gradient with the q / k / v slots given in head layout."""
+    g = torch.zeros_like(qkv)
+    gq, gk, gv = head_parts(g, n_head)
+    for slot, d in ((gq, dq), (gk, dk), (gv, dv)):
+        if d is not None:
+            slot.copy_(d)
+    return g
 
 
-def _context(pd, v):
-    b, nh, s, hd = v.shape
-    return torch.matmul(pd, v).transpose(1, 2).reshape(b, s, nh * hd)
+class _QKScores(torch.autograd.Function):
+    """Causal attention scores q k^T * scale from the FUSED qkv activation.
+
+    Saves qkv itself (operator 3, the reference's [tokens, 3h] QKV matrix,
+    compressed per channel over its 3h columns), not per-head q / k copies."""
+
+    @staticmethod
+    def forward(ctx, qkv, n_head, scale):
+        q, k, _ = head_parts(qkv, n_head)
+        scores = torch.matmul(q, k.transpose(-2, -1)) * scale
+        ctx.save_for_backward(qkv)
+        ctx.n_head, ctx.scale = n_head, scale
+        return scores.masked_fill(_causal(scores.shape[-1], scores.device), float("-inf"))
+
+    @staticmethod
+    def backward(ctx, g):
+        (qkv,) = ctx.saved_tensors
+        q, k, _ = head_parts(qkv, ctx.n_head)
+        g = g.masked_fill(_causal(g.shape[-1], g.device), 0.0) * ctx.scale
+        return _qkv_grad(qkv, ctx.n_head, dq=torch.matmul(g, k), dk=torch.matmul(g.transpose(-2, -1), q)), None, None
+
+
+class _Context(torch.autograd.Function):
+    """probs @ v (v from the fused qkv), heads merged to [b, s, h]; saves the
+    dropped probabilities (operator 6) and qkv (operator 3)."""
+
+    @staticmethod
+    def forward(ctx, pd, qkv, n_head):
+        _, _, v = head_parts(qkv, n_head)
+        ctx.save_for_backward(pd, qkv)
+        ctx.n_head = n_head
+        b, nh, s, hd = v.shape
+        return torch.matmul(pd, v).transpose(1, 2).reshape(b, s, nh * hd)
+
+    @staticmethod
+    def backward(ctx, g):
+        pd, qkv = ctx.saved_tensors
+        _, _, v = head_parts(qkv, ctx.n_head)
+        b, s, h = g.shape
+        g = g.view(b, s, ctx.n_head, h // ctx.n_head).transpose(1, 2)
+        return torch.matmul(g, v.transpose(-2, -1)), _qkv_grad(qkv, ctx.n_head, dv=torch.matmul(pd.transpose(-2, -1), g)), None
+
+
+def _causal_softmax(qkv, n_head, scale, tag=None):
+    return _Softmax.apply(_QKScores.apply(qkv, n_head, scale), tag)
+
+
+def _context(pd, qkv, n_head):
+    return _Context.apply(pd, qkv, n_head)
 
 
 class Block(nn.Module):
@@ -170,13 +201,10 @@ class Block(nn.Module):
         with pol.op(2):
             h = pol.tag(2, self.ln1(x), self.ln1, (x,))
         with pol.op(3):
-            q, k, v = split_heads(self.qkv(h), nh)
-            memo = _Memo(lambda a: split_heads(self.qkv(a), nh))  # one QKV GEMM recomputes all three
-            for i, t in enumerate((q, k, v)):
-                pol.tag(3, t, memo.part(i), (h,))
+            qkv = pol.tag(3, self.qkv(h), self.qkv, (h,))  # saved once, as [tokens, 3h]
         with pol.op(4):
-            fn4 = lambda a, b: _causal_softmax(a, b, self.scale)  # noqa: E731
-            p = _causal_softmax(q, k, self.scale, tag=lambda out: pol.tag(4, out, fn4, (q, k)))
+            fn4 = lambda a: _causal_softmax(a, nh, self.scale)  # noqa: E731
+            p = _causal_softmax(qkv, nh, self.scale, tag=lambda out: pol.tag(4, out, fn4, (qkv,)))
         with pol.op(5):
             mseed = seed * 1000003 + self.layer
             pshape, pdev = tuple(p.shape), p.device
@@ -186,9 +214,10 @@ class Block(nn.Module):
         with pol.op(6):
             fn6 = lambda a, m: a * m / keep  # noqa: E731
             pol.tag(6, pd, fn6, (p, mask))
-            ctx = _context(pd, v)
+            ctx = _context(pd, qkv, nh)
         with pol.op(7):
-            pol.tag(7, ctx, _context, (pd, v))
+            fn7 = lambda a, b: _context(a, b, nh)  # noqa: E731
+            pol.tag(7, ctx, fn7, (pd, qkv))
             fn8 = lambda r, c: r + self.proj(c)  # noqa: E731
             a = pol.tag(8, fn8(x, ctx), fn8, (x, ctx))
         with pol.op(9):

@@ -11,10 +11,14 @@ tensor saved while an operator is running that carries no tag (softmax saving
 its own output) belongs to that operator.
 
 * compress: the tensor's contiguous base is compressed once with the codec
-  ``scheme_for(kind)`` names (codec.py:72-82) through the C-ABI; every view
-  of it (q/k/v of one fused QKV output, transposes) is restored with
-  ``as_strided`` from one shared decompression -- so a fused QKV activation is
-  compressed per channel over its 3h columns exactly like the reference's
+  ``scheme_for(kind)`` names (codec.py:72-82) through the C-ABI, into a
+  pooled :class:`~.slots.CodecSlot` (payload, side buffer, workspace and the
+  outlier prediction allocated once per (operator, occurrence, shape) and
+  reused every step: no allocation, no workspace fill, no synchronisation);
+  every view of it (transposes, strided parts) is restored with
+  ``as_strided`` from one shared decompression.  The model saves the fused
+  QKV output ``[b, s, 3h]`` (gpt.py ``_QKScores`` / ``_Context``), so it is
+  compressed per channel over its 3h columns like the reference's
   ``[tokens, 3h]`` QKV matrix.
 * recompute: the pack hook stores the recipe with its inputs packed under
   their own operators' policies (so a recomputed tensor costs no memory and
@@ -41,6 +45,7 @@ import torch
 
 from . import codec as C
 from .profiles import LayerKind
+from .slots import CodecSlot
 
 RETAIN, COMPRESS, RECOMPUTE = "retain", "compress", "recompute"
 
@@ -55,10 +60,10 @@ class OpInfo:
 class _Base:
     """One packed base storage (compressed or recompute recipe), shared by views."""
 
-    __slots__ = ("kind", "ct", "recipe", "shape", "dtype", "value", "src", "__weakref__")
+    __slots__ = ("kind", "slot", "recipe", "shape", "dtype", "value", "src", "__weakref__")
 
-    def __init__(self, kind, ct, recipe, shape, dtype, src):
-        self.kind, self.ct, self.recipe, self.shape, self.dtype = kind, ct, recipe, shape, dtype
+    def __init__(self, kind, slot, recipe, shape, dtype, src):
+        self.kind, self.slot, self.recipe, self.shape, self.dtype = kind, slot, recipe, shape, dtype
         self.value = None
         self.src = src  # weakref to the packed base tensor: detects address reuse
 
@@ -83,7 +88,11 @@ class ActivationPolicy:
         self._tags: dict[int, tuple] = {}   # storage ptr -> (op_id, recipe)
         self._current: int | None = None
         self._enabled = True
-        self._bases: dict[int, _Base] = {}
+        # storage ptr -> entry; weak: autograd's packed tuples are the only owners,
+        # so a decompressed / recomputed value dies with its last saved tensor
+        self._bases: weakref.WeakValueDictionary = weakref.WeakValueDictionary()
+        self._pool: dict[tuple, CodecSlot] = {}   # (signature, occurrence) -> slot, reused every step
+        self._occ: dict[tuple, int] = {}          # occurrences of a signature in this step
         self.status: torch.Tensor | None = None
         self.records: dict[int, list] = {}  # op_id -> compressed records of the last step (profiling)
         self.measure_kinds: frozenset = frozenset()   # tracking iterations: kinds to count outliers of
@@ -134,6 +143,7 @@ class ActivationPolicy:
     def hooks(self):
         self._tags.clear()
         self._bases.clear()
+        self._occ.clear()
         self.records = {}
         self.measured = {}
         if self.status is None and torch.cuda.is_available():
@@ -207,12 +217,28 @@ class ActivationPolicy:
         k_cap = None
         if spec.scheme is C.Scheme.OUTLIER_SEPARATED:
             k_cap = self.k_caps.get(op_id, max(16, x.shape[1] // 32))
-        ct = C.compress_async(x, spec, k_cap=k_cap, status=self.status)
+        slot = self._slot(op_id, spec, x, k_cap)
+        slot.compress_ptr(x.data_ptr(), torch.cuda.current_stream(x.device).cuda_stream)
         self.stats.compressed += 1
         self.stats.original_bytes += nbytes
-        self.stats.stored_bytes += ct.device_bytes
-        self.records.setdefault(op_id, []).append(ct)
-        return _Base(COMPRESS, ct, None, tuple(base.shape), base.dtype, weakref.ref(base))
+        self.stats.stored_bytes += slot.device_bytes
+        self.records.setdefault(op_id, []).append(slot)
+        return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base))
+
+    def _slot(self, op_id, spec, x, k_cap) -> CodecSlot:
+        """The pooled slot of this (operator, shape, dtype, capacity)'s n-th
+        occurrence in the step (one per layer), created on first use."""
+        sig = (op_id, spec, tuple(x.shape), x.dtype, k_cap)
+        n = self._occ.get(sig, 0)
+        self._occ[sig] = n + 1
+        slot = self._pool.get((sig, n))
+        if slot is None:
+            in_dt = torch.uint8 if x.dtype == torch.bool else x.dtype
+            out_dt = torch.uint8 if spec.scheme is C.Scheme.BIT_MASK else x.dtype
+            slot = CodecSlot(x.shape[0], x.shape[1], spec, in_dt, out_dt, k_cap=k_cap, device=x.device,
+                             status=self.status)
+            self._pool[(sig, n)] = slot
+        return slot
 
     def _materialize(self, entry: _Base) -> torch.Tensor:
         if entry.value is not None:
@@ -225,15 +251,11 @@ class ActivationPolicy:
                 out = fn(*inputs)
             value = out.reshape(entry.shape)
         else:
-            ct = entry.ct
-            if ct.scheme is C.Scheme.BIT_MASK:
-                out = torch.empty((ct.rows, ct.cols), dtype=torch.uint8, device=ct.mask_bits.device)
-                C.decompress_into(ct, out)
-                if entry.dtype == torch.bool:
-                    out = out.view(torch.bool)
-            else:
-                out = torch.empty((ct.rows, ct.cols), dtype=entry.dtype, device=ct.packed_codes.device)
-                C.decompress_into(ct, out)
+            slot = entry.slot
+            out = torch.empty((slot.rows, slot.cols), dtype=slot.out_dtype, device=slot.device)
+            slot.decompress_ptr(out.data_ptr(), torch.cuda.current_stream(out.device).cuda_stream)
+            if entry.dtype == torch.bool:
+                out = out.view(torch.bool)
             value = out.reshape(entry.shape)
         entry.value = value
         return value

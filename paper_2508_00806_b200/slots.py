@@ -95,6 +95,12 @@ class CodecSlot:
         return out
 
     # -- accounting ----------------------------------------------------------
+    @property
+    def device_bytes(self) -> int:
+        """HBM the slot holds for the payload (incl. unused outlier capacity)."""
+        return sum(t.numel() * t.element_size() for t in (self.codes, self.scales, self.offsets, self.idx, self.val)
+                   if t is not None)
+
     def payload_bytes(self, k: int = 0) -> int:
         return _layout(int(self.scheme), self.rows, self.cols, self.group, k)[2]
 

@@ -33,6 +33,42 @@ from .profiles import save_profile
 STRATEGIES = ("retain-all", "full-recompute", "all-compress", "adacc")
 
 
+def model_flops_per_token(cfg: GPTConfig, n_params: int) -> float:
+    """Training FLOPs per token: 6 x parameters (forward + backward of every
+    weight) + 12 x layers x seq x d_model for the attention score / context
+    matmuls (forward 4 L s d, backward twice that).  Recomputation is not
+    counted (it is overhead, not model work)."""
+    return 6.0 * n_params + 12.0 * cfg.n_layer * cfg.seq * cfg.d_model
+
+
+def peak_bf16_flops() -> tuple[float, str]:
+    """Dense bf16 peak the MFU is quoted against: MEASURED_PEAKS.json's sustained
+    cuBLAS figure when present, else the 2.25 PFLOP/s spec."""
+    from pathlib import Path
+    p = Path(__file__).resolve().parent.parent / "MEASURED_PEAKS.json"
+    try:
+        return float(json.loads(p.read_text())["bf16_tflops_sustained"]) * 1e12, "measured sustained cuBLAS bf16"
+    except Exception:
+        return 2.25e15, "B200 dense bf16 spec"
+
+
+def codec_share(tr, batch) -> dict:
+    """One profiled step: device time of the codec kernels (adc::) / all kernels."""
+    torch.cuda.synchronize()
+    with torch.profiler.profile(activities=[torch.profiler.ProfilerActivity.CUDA]) as prof:
+        tr.step(*batch)
+        torch.cuda.synchronize()
+    tot = codec = 0.0
+    for e in prof.events():
+        if e.device_type == torch.autograd.DeviceType.CUDA:
+            us = e.device_time if hasattr(e, "device_time") else e.cuda_time
+            tot += us
+            if "adc::" in e.name:
+                codec += us
+    return {"codec_kernel_us": round(codec, 1), "all_kernel_us": round(tot, 1),
+            "share": round(codec / tot, 4) if tot else 0.0}
+
+
 def plan_for(strategy: str, prof=None) -> dict:
     ids = [o.op_id for o in BLOCK_OPS]
     if strategy == "adacc":
@@ -217,14 +253,24 @@ def run(args) -> dict:
         tokens = args.batch * cfg.seq * world * args.steps
         err = tr.pol.check()
         peak = torch.cuda.max_memory_allocated(dev)
+        lv = [float(l.item()) for l in losses]
+        win = max(1, min(50, len(lv) // 10))
+        tps = tokens / (ms / 1e3)
+        peak_flops, peak_src = peak_bf16_flops()
+        mfu = tps * model_flops_per_token(cfg, tr.model.n_params()) / (world * peak_flops)
+        share = codec_share(tr, tr.batch_at(999)) if getattr(args, "codec_share", False) else None
         out["results"][strategy] = {
-            "plan": plan, "tokens_per_s": tokens / (ms / 1e3), "ms_per_step": ms / args.steps,
-            "peak_bytes": peak, "fits_cap": peak <= cap, "final_loss": float(losses[-1].item()),
-            "mean_loss": statistics.mean(float(l.item()) for l in losses), "device_error_word": err,
+            "plan": plan, "tokens_per_s": tps, "ms_per_step": ms / args.steps,
+            "peak_bytes": peak, "fits_cap": peak <= cap, "final_loss": lv[-1],
+            "smoothed_final_loss": statistics.mean(lv[-win:]), "loss_window": win,
+            "mean_loss": statistics.mean(lv), "mfu": round(mfu, 4), "mfu_peak": peak_src,
+            "codec_share": share, "device_error_word": err,
             "compressed_tensors": tr.pol.stats.compressed, "recomputed_tensors": tr.pol.stats.recomputed,
             "calibration": calib,
         }
-        losses_all[strategy] = [float(l.item()) for l in losses]
+        if getattr(args, "loss_curve", False):
+            out["results"][strategy]["losses"] = [round(v, 5) for v in lv[:: max(1, len(lv) // 100)]]
+        losses_all[strategy] = lv
     return out
 
 
@@ -332,6 +378,8 @@ def main(argv=None):
     ap.add_argument("--policy", default="retain-all,adacc")
     ap.add_argument("--mem-cap-gb", type=float, default=0.0)
     ap.add_argument("--profile-out", default="")
+    ap.add_argument("--codec-share", action="store_true", help="profile one step: codec kernels' share of device time")
+    ap.add_argument("--loss-curve", action="store_true", help="include a subsampled loss curve per strategy")
     ap.add_argument("--evolve", type=int, default=0, help="config 5: N iterations of policy evolution")
     ap.add_argument("--max-interval", type=int, default=64)
     ap.add_argument("--settle", type=int, default=150)

@@ -78,3 +78,55 @@ def test_int8_nonfinite_raises():
     x[2, 7] = float("inf")
     with pytest.raises(adc.NonFiniteInputError):
         adc.quantize_int8(x)
+
+
+# ---------------------------------------------------------------- int4 with float32 scales
+def test_int4f32_oracle_equals_reference_when_scales_are_f16_exact(reference_codec):
+    """Where max|h|/8 is exactly a float16 the float32-scale codec must write
+    the reference's own int4 codes (only the scale's storage differs)."""
+    rng = np.random.default_rng(5)
+    x = rng.normal(size=(32, 256)).astype(np.float16).astype(np.float32)
+    x.reshape(-1, 128)[:, 0] = 8.0  # group maxima 8 -> s = 1 (f16-exact)
+    ct = I8.quantize_int4_f32(x, 128)
+    ref = reference_codec.quantize_symmetric(x, 128)
+    assert np.array_equal(ct.codes, np.frombuffer(ref.packed_codes, np.uint8))
+    assert np.array_equal(ct.scales, ref.scales.astype(np.float32))
+
+
+def test_int4f32_oracle_properties():
+    rng = np.random.default_rng(1)
+    x = rng.normal(size=(48, 80)).astype(np.float32) * 3e-3  # scales below the f16 normal range
+    ct = I8.quantize_int4_f32(x, 16)
+    h = x.astype(np.float16).astype(np.float32).reshape(-1, 16)
+    top = np.abs(h).max(axis=1)
+    assert np.array_equal(ct.scales, (top / 8).astype(np.float32))  # not rounded to f16
+    err = np.abs(I8.dequantize_int4_f32(ct).reshape(-1, 16) - h)
+    # half a step, except the +8 s quotient of a positive maximum, clipped to 7 (codec.py:231)
+    bound = np.where(h >= 7.5 * ct.scales[:, None], ct.scales[:, None], 0.5 * ct.scales[:, None])
+    assert np.all(err <= bound * (1 + 2**-20) + 1e-30)
+    assert ct.codes.size == (48 * 80 + 1) // 2
+
+
+CASES4 = [((256, 768), 128, "float32"), ((8192, 1024), 128, "bfloat16"), ((1000, 40), 8, "float16"),
+          ((333, 1024), 64, "bfloat16"), ((7, 13), 5, "float32"), ((64, 4096), 256, "float16"),
+          ((3, 1), 1, "float32"), ((5, 7), 3, "bfloat16")]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,group,dtype_name", CASES4)
+def test_int4f32_device_matches_oracle(shape, group, dtype_name):
+    import torch
+    import paper_2508_00806_b200 as adc
+    rng = np.random.default_rng(shape[0] + 7 * group)
+    x = rng.normal(size=shape).astype(np.float32) * 3
+    x[:, :: max(1, shape[1] // 7)] *= 25
+    x[0, : min(8, shape[1])] = 0.0
+    xt = torch.from_numpy(x).to(getattr(torch, dtype_name))
+    want = I8.quantize_int4_f32(xt.to(torch.float32).numpy(), group)
+    ct = adc.quantize_int4_f32(xt.cuda(), group)
+    np.testing.assert_array_equal(ct.codes.cpu().numpy(), want.codes)
+    np.testing.assert_array_equal(ct.scales.cpu().numpy().view(np.uint32), want.scales.view(np.uint32))
+    y = adc.dequantize_int4_f32(ct).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), I8.dequantize_int4_f32(want).view(np.uint32))
+    n = shape[0] * shape[1]
+    assert ct.compressed_size_bytes == (n + 1) // 2 + 4 * -(-n // group)
