@@ -335,9 +335,10 @@ static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols) {
   }
   const int64_t gx = (cols + kStripCols - 1) / kStripCols;
   int64_t gy = static_cast<int64_t>(c.num_sms) * occ / gx;  // never a partial second wave
-  // at least 8 rows per thread, so its 8 loads go out together (a full wave of
-  // CTAs with ~7 rows each leaves every thread on one load at a time)
-  const int64_t maxy = (rows + 8 * kRowLanes - 1) / (8 * kRowLanes);
+  // (measured: capping the grid so every thread holds a full batch of 8 rows
+  // was faster in isolation but slower inside the bench step, 15.1 -> 18.7 us
+  // at [8192, 1024] cold; the full wave stays)
+  const int64_t maxy = (rows + kRowLanes - 1) / kRowLanes;
   if (gy > maxy) gy = maxy;
   if (gy < 1) gy = 1;
   if (gy > 65535) gy = 65535;
