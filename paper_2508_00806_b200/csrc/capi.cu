@@ -80,10 +80,9 @@ size_t workspace_layout(int64_t cols, Workspace *ws, void *base) {
   w.node_n = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_left = reinterpret_cast<int32_t *>(take(sizeof(int32_t) * nodes));
   w.node_val = reinterpret_cast<double *>(take(sizeof(double) * nodes));
-  const int64_t vcols = cols < 256 ? 256 : cols;  // narrow matrices stream as 256-column views (outlier.cu)
-  w.acc = reinterpret_cast<double *>(take(sizeof(double) * vcols));
+  w.acc = reinterpret_cast<double *>(take(sizeof(double) * cols));
   w.k4acc = reinterpret_cast<double *>(take(sizeof(double) * 2 * cols));
-  w.macc = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * vcols));
+  w.macc = reinterpret_cast<uint32_t *>(take(sizeof(uint32_t) * cols));
   w.pflag = reinterpret_cast<uint8_t *>(take(static_cast<size_t>(cols) + 8));
   w.bytes = off;
   if (ws) *ws = w;

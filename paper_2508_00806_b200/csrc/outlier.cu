@@ -56,9 +56,7 @@ __device__ __forceinline__ double h_hi_f64(uint32_t w) {
 }
 
 struct ColArgs {
-  int64_t rows, cols;   // the matrix stage A streams (a narrow matrix is viewed as wider, below)
-  int64_t rrows, rcols; // the real matrix: rrows = rows * vfold, rcols * vfold = cols
-  int vfold;            // virtual columns per real column (1, or 256 / rcols for narrow matrices)
+  int64_t rows, cols;
   double *acc;          // [cols] f64 sum accumulators, zero at rest
   uint32_t *macc;       // [cols] u32 max accumulators, zero at rest
   double *S;            // column sums (sum mode)
@@ -104,8 +102,29 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
   uint32_t mx[4] = {0, 0, 0, 0};
   if (live) {
     const int64_t step = static_cast<int64_t>(gridDim.y) * kRowLanes;
-    auto accumulate = [&](const uint4 &hv) {
-      const uint32_t w[4] = {hv.x, hv.y, hv.z, hv.w};
+    int64_t r = static_cast<int64_t>(blockIdx.y) * kRowLanes + ty;
+    for (; r + 7 * step < rows; r += 8 * step) {
+      uint4 h[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) h[q] = Loader<DT>::template load8<true>(x, (r + q * step) * cols + cu * 8);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const uint32_t w[4] = {h[q].x, h[q].y, h[q].z, h[q].w};
+        if (SUM) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            acc[2 * j] = __dadd_rn(acc[2 * j], fabs(h_lo_f64(w[j])));
+            acc[2 * j + 1] = __dadd_rn(acc[2 * j + 1], fabs(h_hi_f64(w[j])));
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) mx[j] = __vmaxu2(mx[j], w[j] & 0x7fff7fffu);
+        }
+      }
+    }
+    for (; r < rows; r += step) {
+      const uint4 h = Loader<DT>::template load8<true>(x, r * cols + cu * 8);
+      const uint32_t w[4] = {h.x, h.y, h.z, h.w};
       if (SUM) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -116,16 +135,7 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
 #pragma unroll
         for (int j = 0; j < 4; ++j) mx[j] = __vmaxu2(mx[j], w[j] & 0x7fff7fffu);
       }
-    };
-    int64_t r = static_cast<int64_t>(blockIdx.y) * kRowLanes + ty;
-    for (; r + 7 * step < rows; r += 8 * step) {
-      uint4 h[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) h[q] = Loader<DT>::template load8<true>(x, (r + q * step) * cols + cu * 8);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) accumulate(h[q]);
     }
-    for (; r < rows; r += step) accumulate(Loader<DT>::template load8<true>(x, r * cols + cu * 8));
   }
   if (SUM) {
 #pragma unroll
@@ -164,34 +174,23 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
     s_last = atom_add_acq_rel_gpu(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   if (!s_last) return;
-  // move the accumulators out (4 columns per thread per round trip) and reset
-  // them; a narrow matrix folds its vfold virtual columns per real column
-  // (any order: the sums are exact below 2^29, the maxima are order-free)
-  const int64_t rc = a.rcols;
-  const bool s_smem = SUM && rc <= kSmemSumCols;
+  // move the accumulators out (4 columns per thread per round trip) and reset them
+  const bool s_smem = SUM && cols <= kSmemSumCols;
   double *s_S = reinterpret_cast<double *>(s_buf);
   int flagged = 0;
-  for (int64_t base = 0; base < rc; base += 4 * kThreads) {
+  for (int64_t base = 0; base < cols; base += 4 * kThreads) {
     if (SUM) {
       double v[4];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
-        v[q] = c < rc ? __ldcg(a.acc + c) : 0.0;  // (4 loads in flight)
+        v[q] = c < cols ? __ldcg(a.acc + c) : 0.0;
       }
-      if (a.vfold > 1)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t c = base + q * kThreads + threadIdx.x;
-          if (c < rc)
-            for (int j = 1; j < a.vfold; ++j) v[q] = __dadd_rn(v[q], __ldcg(a.acc + j * rc + c));
-        }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
-        if (c < rc) {
+        if (c < cols) {
           __stcg(a.acc + c, 0.0);
-          for (int j = 1; j < a.vfold; ++j) __stcg(a.acc + j * rc + c, 0.0);
           __stcg(a.S + c, v[q]);
           if (s_smem) s_S[c] = v[q];
           flagged |= !(v[q] < kExactLimit);
@@ -202,21 +201,13 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
-        m[q] = c < rc ? __ldcg(a.macc + c) : 0u;  // (4 loads in flight)
+        m[q] = c < cols ? __ldcg(a.macc + c) : 0u;
       }
-      if (a.vfold > 1)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int64_t c = base + q * kThreads + threadIdx.x;
-          if (c < rc)
-            for (int j = 1; j < a.vfold; ++j) m[q] = max(m[q], __ldcg(a.macc + j * rc + c));
-        }
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
-        if (c < rc) {
+        if (c < cols) {
           __stcg(a.macc + c, 0u);
-          for (int j = 1; j < a.vfold; ++j) __stcg(a.macc + j * rc + c, 0u);
           __stcg(a.colmax + c, m[q]);
           flagged |= m[q] >= 0x7c00u;
         }
@@ -230,18 +221,18 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
     return;
   }
   if (flagged) {  // some total >= 2^29: numpy's row order
-    numpy_order_sums<DT>(x, a.rrows, rc, a.S);
+    numpy_order_sums<DT>(x, rows, cols, a.S);
     __syncthreads();
     if (s_smem)
-      for (int64_t c = threadIdx.x; c < rc; c += kThreads) s_S[c] = __ldcg(a.S + c);
+      for (int64_t c = threadIdx.x; c < cols; c += kThreads) s_S[c] = __ldcg(a.S + c);
     __syncthreads();
   }
   if (a.do_stats) {
     if (s_smem)
-      outlier_stats_block<true>(s_S, a.rrows, rc, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
+      outlier_stats_block<true>(s_S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
                                 a.err, a.too_many_check != 0, s_buf + kSmemSumCols * 8);
     else
-      outlier_stats_block<false>(a.S, a.rrows, rc, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
+      outlier_stats_block<false>(a.S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
                                  a.err, a.too_many_check != 0, s_buf);
   }
 }
@@ -292,23 +283,10 @@ __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restr
     default: return -1;                                              \
   }
 
-// A narrow matrix (cols < 256 dividing 256, rows a multiple of 256 / cols)
-// is streamed as the contiguous [rows / V, 256] matrix whose column c' holds
-// real column c' % cols: full 256-column strips instead of 24 idle lanes of
-// 32 at cols = 64 (per-head q/k/v); the final stage folds the V partials.
-static int narrow_fold(int64_t rows, int64_t cols) {
-  if (cols >= kStripCols || kStripCols % cols || cols % 8) return 1;
-  const int v = static_cast<int>(kStripCols / cols);
-  return rows % v == 0 ? v : 1;
-}
-
 static ColArgs make_args(int64_t rows, int64_t cols, const Workspace &ws) {
   ColArgs a{};
-  a.vfold = narrow_fold(rows, cols);
-  a.rrows = rows;
-  a.rcols = cols;
-  a.rows = rows / a.vfold;
-  a.cols = cols * a.vfold;
+  a.rows = rows;
+  a.cols = cols;
   a.acc = ws.acc;
   a.macc = ws.macc;
   a.S = ws.colsum;
@@ -335,9 +313,6 @@ static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols) {
   }
   const int64_t gx = (cols + kStripCols - 1) / kStripCols;
   int64_t gy = static_cast<int64_t>(c.num_sms) * occ / gx;  // never a partial second wave
-  // (measured: capping the grid so every thread holds a full batch of 8 rows
-  // was faster in isolation but slower inside the bench step, 15.1 -> 18.7 us
-  // at [8192, 1024] cold; the full wave stays)
   const int64_t maxy = (rows + kRowLanes - 1) / kRowLanes;
   if (gy > maxy) gy = maxy;
   if (gy < 1) gy = 1;
@@ -358,12 +333,11 @@ int launch_colstats_sum(const Ctx &c, const void *x, int dt, int64_t rows, int64
   a.err = err;
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
-      const dim3 g = col_grid(c, colreduce<DT, true>, a.rows, a.cols);
+      const dim3 g = col_grid(c, colreduce<DT, true>, rows, cols);
       launch_k(colreduce<DT, true>, g, kThreads, 0, c.stream, x, a);
       note_launches(1);
     });
   } else {
-    a.vfold = 1, a.rows = rows, a.cols = cols;
     const int g = static_cast<int>((cols + kThreads - 1) / kThreads);
     ADC_DT_SWITCH(dt, DT, (launch_k(colstats_generic<DT, true>, g, kThreads, 0, c.stream, x, a), note_launches(1)));
   }
@@ -376,12 +350,11 @@ int launch_colstats_max(const Ctx &c, const void *x, int dt, int64_t rows, int64
   a.err = err;
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
-      const dim3 g = col_grid(c, colreduce<DT, false>, a.rows, a.cols);
+      const dim3 g = col_grid(c, colreduce<DT, false>, rows, cols);
       launch_k(colreduce<DT, false>, g, kThreads, 0, c.stream, x, a);
       note_launches(1);
     });
   } else {
-    a.vfold = 1, a.rows = rows, a.cols = cols;
     const int g = static_cast<int>((cols + kThreads - 1) / kThreads);
     ADC_DT_SWITCH(dt, DT, (launch_k(colstats_generic<DT, false>, g, kThreads, 0, c.stream, x, a), note_launches(1)));
   }
