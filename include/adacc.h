@@ -123,6 +123,12 @@ ADC_API unsigned long long adc_kernel_launches(void);
  *                   automatic (default: the single pass for tall tensors of
  *                   <= 1024 columns, >= 2^25 elements, where it measured
  *                   faster).  Also ADC_OUTLIER_PATH=0/1/2.
+ *   "outlier_decompress"  0 = dequantiser launch + outlier overwrite launch,
+ *                   2 = one launch (output tiles dequantised into shared
+ *                   memory, overwritten there, stored whole) wherever
+ *                   eligible (default).
+ *   "outlier_tile"  elements per tile of that launch: 4096, 8192 (default)
+ *                   or 16384.
  *   "k4_trace"      1 = record the single-pass kernel's phase timestamps.
  *   "k4_dbg"        timing experiments only (1 = stop the single pass after
  *                   its streaming phase; results invalid).

@@ -120,6 +120,14 @@ int adc_set_option(const char *key, int value) {
     set_k4_mode(value);
     return ADC_OK;
   }
+  if (k == "outlier_decompress") {  // 0: dequantise + overwrite launches, 2: one launch where eligible (default)
+    set_outlier_decompress_mode(value);
+    return ADC_OK;
+  }
+  if (k == "outlier_tile") {  // elements per tile of the one-launch outlier decompress: 4096, 8192 (default), 16384
+    set_outlier_tile(value);
+    return ADC_OK;
+  }
   if (k == "k4_dbg") {  // timing experiments on the single-pass kernel (results invalid when != 0)
     set_k4_dbg(value);
     return ADC_OK;
@@ -246,6 +254,10 @@ int adc_decompress(int scheme, const uint8_t *codes, const uint16_t *scales,
   if (asym && !offsets) return fail(ADC_EINVAL, "null offsets");
   const bool pc = group_size == ADC_PER_CHANNEL;
   int rc = 0;
+  if (scheme == ADC_OUTLIER_SEPARATED && k_cap > 0 && !pc && outlier_idx && outlier_val && k_dev &&
+      launch_outlier_decompress_tiles(c, codes, scales, outlier_idx, outlier_val, k_dev, k_cap, rows, cols,
+                                     group_size, y, out_dtype) == 0)
+    return check_launch("decompress");
   if (pc && !asym && channel_fast_ok(y, rows, cols, codes, scales) &&
       reinterpret_cast<uintptr_t>(y) % 16 == 0) {
     rc = launch_channel_decompress(c, codes, scales, rows, cols, y, out_dtype);

@@ -533,6 +533,101 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
+// Outlier-separated decompress in ONE launch (codec.py:276-285).  Each CTA
+// owns a TILE of the row-major output (T elements): it dequantises the tile's
+// 8-element units into shared memory, overwrites the flagged channels of the
+// rows the tile spans there (the side-buffer values were requested before the
+// dequantisation, so their latency overlaps it), and streams the finished
+// tile out with full 128-bit stores -- no 2-byte scatter into global memory,
+// hence no partial-sector writes at any output size.
+template <int OT>
+__device__ __forceinline__ void put8_shared(unsigned char *t, const float *v) {
+  if constexpr (OT == ADC_F32) {
+    reinterpret_cast<uint4 *>(t)[0] = make_uint4(__float_as_uint(v[0]), __float_as_uint(v[1]),
+                                                 __float_as_uint(v[2]), __float_as_uint(v[3]));
+    reinterpret_cast<uint4 *>(t)[1] = make_uint4(__float_as_uint(v[4]), __float_as_uint(v[5]),
+                                                 __float_as_uint(v[6]), __float_as_uint(v[7]));
+  } else if constexpr (OT == ADC_BF16) {
+    *reinterpret_cast<uint4 *>(t) = make_uint4(pack_bf2(v[0], v[1]), pack_bf2(v[2], v[3]),
+                                               pack_bf2(v[4], v[5]), pack_bf2(v[6], v[7]));
+  } else {
+    *reinterpret_cast<uint4 *>(t) = make_uint4(f32x2_to_h2(v[0], v[1]), f32x2_to_h2(v[2], v[3]),
+                                               f32x2_to_h2(v[4], v[5]), f32x2_to_h2(v[6], v[7]));
+  }
+}
+
+template <int OT>
+__device__ __forceinline__ void put1_shared(unsigned char *t, float v) {
+  if constexpr (OT == ADC_F32) *reinterpret_cast<float *>(t) = v;
+  else if constexpr (OT == ADC_BF16) *reinterpret_cast<__nv_bfloat16 *>(t) = __float2bfloat16_rn(v);
+  else *reinterpret_cast<__half *>(t) = __float2half_rn(v);
+}
+
+template <int OT, int L, int T>
+__global__ void __launch_bounds__(kThreads)
+    outlier_dequant_tiles(const uint32_t *__restrict__ codes, const uint16_t *__restrict__ scales,
+                          int64_t rows, int64_t cols, int64_t n, const uint32_t *__restrict__ idx,
+                          const uint16_t *__restrict__ val, const int32_t *__restrict__ k_dev, int k_cap,
+                          void *__restrict__ y) {
+  constexpr int OSZ = OT == ADC_F32 ? 4 : 2;
+  constexpr int UPT = T / 8 / kThreads;  // 8-element units per thread
+  constexpr int PF = 2;                  // side-buffer pairs prefetched per thread
+  __shared__ __align__(16) unsigned char tile[T * OSZ];
+  pdl_entry();
+  const int64_t e0 = static_cast<int64_t>(blockIdx.x) * T;
+  const int te = static_cast<int>(min(n - e0, static_cast<int64_t>(T)));  // multiple of 8
+  const int kk = min(__ldg(k_dev), k_cap);
+  uint32_t w[UPT];
+#pragma unroll
+  for (int q = 0; q < UPT; ++q) {
+    const int lu = q * kThreads + threadIdx.x;
+    w[q] = lu * 8 < te ? __ldcs(codes + (e0 >> 3) + lu) : 0u;
+  }
+  const int64_t ra = e0 / cols;
+  const int nr = static_cast<int>((e0 + te - 1) / cols - ra + 1);
+  const int pairs = kk * nr;
+  uint32_t pc[PF];
+  uint16_t pv[PF];
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int p = threadIdx.x + i * kThreads;
+    if (p < pairs) {
+      const int j = p / nr, rr = p - j * nr;
+      pc[i] = __ldg(idx + j);
+      pv[i] = __ldg(val + static_cast<int64_t>(j) * rows + ra + rr);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < UPT; ++q) {
+    const int lu = q * kThreads + threadIdx.x;
+    if (lu * 8 >= te) continue;
+    const float s = h2f(__ldg(scales + ((e0 >> 3) + lu) / L));
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = deq<false>(nib_code(w[q], j), s, 0.f);
+    put8_shared<OT>(tile + lu * 8 * OSZ, v);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < PF; ++i) {
+    const int p = threadIdx.x + i * kThreads;
+    if (p < pairs) {
+      const int j = p / nr, rr = p - j * nr;
+      const int64_t e = (ra + rr) * cols + pc[i] - e0;
+      if (e >= 0 && e < te) put1_shared<OT>(tile + e * OSZ, h2f(pv[i]));
+    }
+  }
+  for (int p = threadIdx.x + PF * kThreads; p < pairs; p += kThreads) {
+    const int j = p / nr, rr = p - j * nr;
+    const int64_t e = (ra + rr) * cols + __ldg(idx + j) - e0;
+    if (e >= 0 && e < te) put1_shared<OT>(tile + e * OSZ, h2f(__ldg(val + static_cast<int64_t>(j) * rows + ra + rr)));
+  }
+  __syncthreads();
+  char *dst = static_cast<char *>(y) + e0 * OSZ;
+  for (int off = threadIdx.x * 16; off < te * OSZ; off += kThreads * 16)
+    st_stream16(dst + off, *reinterpret_cast<const uint4 *>(tile + off));
+}
+
 // Outlier overwrite after the plain dequantisation (codec.py:284-285), one
 // thread per (rank, row) rewriting the whole 32-byte sector that holds the
 // flagged element: 16 dequantised values (their 128-group's scale; sectors
@@ -836,6 +931,44 @@ int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *
       launch_k(group_dequant_generic<OT, false>, grid, kThreads, 0, c.stream, codes, scales, nullptr,
                                                                         n, g, pc, rows, cols, y), note_launches(1);
   });
+  return 0;
+}
+
+static int g_outlier_decompress_mode = 2;  // 0: dequantise + overwrite launches, 2: one launch
+static int g_outlier_tile = 8192;          // elements per tile of the one-launch decompress
+void set_outlier_decompress_mode(int m) { g_outlier_decompress_mode = m; }
+void set_outlier_tile(int t) { g_outlier_tile = t; }
+
+int launch_outlier_decompress_tiles(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                                    const uint32_t *idx, const uint16_t *val, const int32_t *k_dev,
+                                    int64_t k_cap, int64_t rows, int64_t cols, int64_t g, void *y,
+                                    int ot) {
+  if (g_outlier_decompress_mode == 0 || k_cap <= 0) return 1;
+  const int L = lanes_for_group(g, 8);
+  const int64_t n = rows * cols;
+  if (L == 0 || n % 8 != 0 || !aligned(y, 16) || !aligned(codes, 4) || k_cap > (1 << 22) ||
+      n >= (1ll << 40))
+    return 1;
+  const int T = g_outlier_tile;
+  // pairs per tile = k x rows spanned must stay in int
+  if ((static_cast<int64_t>(T) / cols + 2) * k_cap >= (1ll << 31)) return 1;
+  const int64_t tiles = (n + T - 1) / T;
+  if (tiles >= (1ll << 31)) return 1;
+  const uint32_t *codes32 = reinterpret_cast<const uint32_t *>(codes);
+#define ADC_TILES(TT)                                                                                  \
+  ADC_OT_SWITCH(ot, OT, ADC_L_SWITCH(L, LL, {                                                          \
+    constexpr int TS = (OT == ADC_F32 && TT > 8192) ? 8192 : TT; /* static smem <= 48 KB */           \
+    launch_k(outlier_dequant_tiles<OT, LL, TS>, static_cast<int>((n + TS - 1) / TS), kThreads, 0,     \
+             c.stream, codes32, scales, rows, cols, n, idx, val, k_dev, static_cast<int>(k_cap), y);  \
+    note_launches(1);                                                                                  \
+  }))
+  switch (T) {
+    case 4096: ADC_TILES(4096); break;
+    case 8192: ADC_TILES(8192); break;
+    case 16384: ADC_TILES(16384); break;
+    default: return 1;
+  }
+#undef ADC_TILES
   return 0;
 }
 

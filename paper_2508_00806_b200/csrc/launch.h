@@ -81,6 +81,13 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
 int launch_group_decompress(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
                             const uint16_t *offsets, int64_t rows, int64_t cols, int64_t g,
                             bool asym, void *y, int ot);
+// one-launch outlier decompress (shared-memory tiles); returns 1 when not eligible
+int launch_outlier_decompress_tiles(const Ctx &c, const uint8_t *codes, const uint16_t *scales,
+                                   const uint32_t *idx, const uint16_t *val, const int32_t *k_dev,
+                                   int64_t k_cap, int64_t rows, int64_t cols, int64_t g, void *y,
+                                   int ot);
+void set_outlier_decompress_mode(int m);
+void set_outlier_tile(int t);
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,
                            void *y, int ot, const uint8_t *codes = nullptr,

@@ -55,12 +55,25 @@ class _Recorder(ActivationPolicy):
         return t
 
 
+_FLUSH: torch.Tensor | None = None
+
+
 def _time(fn, reps: int) -> float:
+    """Median device time of one ``fn()``: L2 flushed before each rep, and a
+    device-side sleep queued ahead of the start event so the host has
+    submitted ``fn``'s kernels before the GPU reaches them -- the measured
+    interval is kernel time, not host launch latency (which a training step,
+    where the host runs ahead of the device, never sees)."""
+    global _FLUSH
+    if _FLUSH is None:
+        _FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # 2x L2
     for _ in range(2):
         fn()
     ts = []
     for _ in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        _FLUSH.zero_()
+        torch.cuda._sleep(1_000_000)  # ~0.5 ms of device time for the host to enqueue fn
         a.record()
         fn()
         b.record()

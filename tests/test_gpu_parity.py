@@ -439,6 +439,57 @@ def test_outlier_decompress_sector_patch_large_outputs(torch_cuda, rows):
     assert torch.equal(y32.view(torch.int32), ref.view(torch.int32))
 
 
+@pytest.mark.parametrize("out_name", ["float32", "bfloat16", "float16"])
+@pytest.mark.parametrize("shape,group,n_hot,k_cap", [
+    ((8192, 1024), 128, 11, 32), ((2048, 4096), 128, 40, 128), ((777, 896), 64, 9, 16),
+    ((5000, 128), 128, 3, 8), ((300, 8), 16, 1, 4), ((4096, 1024), 128, 0, 32),
+    ((2048, 768), 128, 20, 8), ((64, 4096), 256, 5, 16), ((16384 + 256, 4096), 128, 37, 64)])
+def test_outlier_decompress_one_launch_vs_two(torch_cuda, shape, group, n_hot, k_cap, out_name):
+    """The one-launch outlier decompress (output tiles dequantised into shared
+    memory and overwritten there, every tile size) writes the same bytes as
+    the dequantiser + overwrite launches and the oracle: ragged last row block, k = 0, k above
+    the slot's capacity (the first k_cap outliers exact), every output dtype,
+    and an output past L2 (where the two-launch path takes the sector patch)."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200 import _lib
+    from paper_2508_00806_b200.slots import CodecSlot
+    rows, cols = shape
+    g = torch.Generator(device="cuda").manual_seed(rows + cols + n_hot)
+    x = torch.randn(rows, cols, device="cuda", generator=g)
+    if n_hot:
+        x[:, torch.randperm(cols, generator=g, device="cuda")[:n_hot]] *= 40
+    x = x.to(torch.bfloat16)
+    out_dt = getattr(torch, out_name)
+    slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED, group), torch.bfloat16, out_dt,
+                     k_cap=k_cap)
+    slot.compress(x)
+    outs = {}
+    try:
+        for mode, tile in ((0, 8192), (2, 4096), (2, 16384), (2, 8192)):
+            _lib.set_option("outlier_decompress", mode)
+            _lib.set_option("outlier_tile", tile)
+            torch.cuda.synchronize()
+            n0 = _lib.lib().adc_kernel_launches()
+            outs[(mode, tile)] = slot.decompress()
+            torch.cuda.synchronize()
+            launches = _lib.lib().adc_kernel_launches() - n0
+            assert launches == (1 if mode == 2 else 2)
+    finally:
+        _lib.set_option("outlier_decompress", 2)
+        _lib.set_option("outlier_tile", 8192)
+    for key, out in outs.items():
+        assert torch.equal(outs[(0, 8192)].view(torch.uint8), out.view(torch.uint8)), key
+    outs[2] = outs[(2, 8192)]
+    if rows * cols <= (1 << 22):
+        k_true = int(slot.k_status[1])
+        assert k_true == n_hot or n_hot < 3  # (8 columns: z > 3 is unreachable)
+        want, wdeq = oracle_run(x.cpu().to(torch.float32).numpy(), cases.OUTL, group, 3.0)
+        if k_true <= k_cap:
+            ref = torch.from_numpy(wdeq).to(out_dt)
+            assert torch.equal(outs[2].cpu().view(torch.uint8), ref.view(torch.uint8))
+
+
 @pytest.mark.parametrize("shape,dtype_name", [((512, 1024), "bfloat16"), ((1000, 40), "float32"),
                                               ((257, 4096), "float16")])
 def test_outlier_gather_modes_vs_oracle(torch_cuda, shape, dtype_name, monkeypatch):
