@@ -105,6 +105,8 @@ const char *adc_last_error(void) { return g_last_error.c_str(); }
 
 unsigned long long adc_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
+static int g_trace_src = 0;  // adc_debug_trace_k4 source: 0 single pass, 1 column statistics
+
 int adc_set_option(const char *key, int value) {
   if (!key) return fail(ADC_EINVAL, "null option key");
   const std::string k(key);
@@ -132,6 +134,11 @@ int adc_set_option(const char *key, int value) {
     set_k4_dbg(value);
     return ADC_OK;
   }
+  if (k == "cr_trace") {  // record phase timestamps of the column-statistics kernel (adc_debug_trace_k4 reads them)
+    set_cr_trace(value);
+    g_trace_src = value ? 1 : 0;
+    return ADC_OK;
+  }
   if (k == "k4_trace") {  // record phase timestamps of the single-pass kernel (adc_debug_trace_k4)
     set_k4_trace(value);
     return ADC_OK;
@@ -142,7 +149,7 @@ int adc_set_option(const char *key, int value) {
 
 int adc_debug_trace_k4(unsigned long long *out, int n) {
   if (!out || n < 0) return fail(ADC_EINVAL, "bad trace buffer");
-  const int r = read_k4_trace(out, n);
+  const int r = g_trace_src == 1 ? read_cr_trace(out, n) : read_k4_trace(out, n);
   return r < 0 ? fail(ADC_ECUDA, "trace copy failed") : r;
 }
 

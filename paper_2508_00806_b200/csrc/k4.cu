@@ -861,17 +861,18 @@ __global__ void __launch_bounds__(kOT, 1) outlier_onepass(OArgs a) {
     const int c1 = static_cast<int>(min(cols, static_cast<int64_t>(c0 + run)));
     uint32_t fb = 0;
     if (sigma != 0.0) {
-      // z = (s - mean) / sigma (numpy); q = (s - mean) * (1 / sigma) is within
-      // 2^-50 relative of z, so it decides every column outside a 2^-46
-      // relative margin around thr; inside it, the correctly rounded division
-      const double rsig = __drcp_rn(sigma);
-      const double hi = __dmul_rn(a.thr, 1.0 + 0x1p-46), lo = __dmul_rn(a.thr, 1.0 - 0x1p-46);
-#pragma unroll 1
+      // z = fl(d / sigma), d = fl(s - mean) (numpy), is monotone in d: decided
+      // in the d domain against T = fl(thr * sigma) outside a |T| * 2^-46
+      // margin (far beyond the quotient's rounding), the correctly rounded
+      // division inside it (stats.cuh, outlier_flags_block)
+      const double T = __dmul_rn(a.thr, sigma);
+      const double T_m = __dadd_rn(__dmul_rn(fabs(T), 0x1p-46), 0x1p-1000);
+      const double T_hi = __dadd_rn(T, T_m), T_lo = __dsub_rn(T, T_m);
+#pragma unroll 4
       for (int c = c0; c < c1; ++c) {
         const double d = __dsub_rn(S[c], mean);
-        const double q = __dmul_rn(d, rsig);
-        bool f = q > fmax(hi, lo) + 0x1p-1000;
-        if (!f && q >= fmin(hi, lo) - 0x1p-1000) f = __ddiv_rn(d, sigma) > a.thr;
+        bool f = d > T_hi;
+        if (!f && !(d < T_lo)) f = __ddiv_rn(d, sigma) > a.thr;
         fb |= (f ? 1u : 0u) << (c - c0);
       }
     }

@@ -32,6 +32,7 @@
 #include "stats.cuh"
 
 #include <atomic>
+#include <mutex>
 #include <cstdlib>
 
 namespace adc {
@@ -39,8 +40,14 @@ namespace adc {
 constexpr double kExactLimit = 536870912.0;  // 2^29
 constexpr int kStripCols = 256;              // 32 column units of 8 per CTA
 constexpr int kRowLanes = kThreads / 32;     // 8
-constexpr int kSmemSumCols = 4096;           // the final CTA keeps S in shared memory up to here
-constexpr int kTailSmem = kSmemSumCols * 8 + kStatsScratch;
+constexpr int kSmemSumCols = 8192;           // the final CTA keeps S in shared memory up to here
+constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
+// dynamic shared memory of a launch: the stage A fold buffer, or (sum mode,
+// cols <= kSmemSumCols) the column sums + the statistics scratch for the tail
+static inline int col_smem(bool sum, int64_t cols) {
+  const int64_t tail = (sum && cols <= kSmemSumCols) ? ((cols * 8 + 15) & ~int64_t{15}) + kStatsScratch : 0;
+  return static_cast<int>(tail > kStageASmem ? tail : (kStageASmem > kStatsScratch ? kStageASmem : kStatsScratch));
+}
 
 // f16 half of a packed word -> f64 in one F2F.F64.F16 (reads .H0/.H1 directly;
 // keeps the integer pipe free -- the bit-trick version was ALU-bound).
@@ -66,12 +73,33 @@ struct ColArgs {
   int do_stats, too_many_check;
   double thr;
   int64_t k_cap;
+  int trace;  // record phase timestamps (tuning, "cr_trace")
   Tree tree;
   uint8_t *flag;
   uint32_t *idx;
   int32_t *k_out;
   uint32_t *err;
 };
+
+// Phase timestamps of the last traced launch (tuning): per CTA [0] entry,
+// [1] stage A done, [2] arrival; then at kCrTraceCtas * 4: the last CTA's
+// [0] tail start, [1] accumulators moved, [2] statistics done.
+constexpr int kCrTraceCtas = 4096;
+__device__ unsigned long long g_crtrace[kCrTraceCtas * 4 + 16];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define CR_TRACE(slot)                                                                         \
+  do {                                                                                         \
+    const int cta_ = blockIdx.y * gridDim.x + blockIdx.x;                                      \
+    if (a.trace && threadIdx.x == 0 && cta_ < kCrTraceCtas) g_crtrace[cta_ * 4 + (slot)] = gtimer(); \
+  } while (0)
+#define CR_TRACE_TAIL(slot)                                                                    \
+  do {                                                                                         \
+    if (a.trace && threadIdx.x == 0) g_crtrace[kCrTraceCtas * 4 + (slot)] = gtimer();          \
+  } while (0)
 
 // numpy's row-order float64 column sums (only when some total >= 2^29)
 template <int DT>
@@ -88,14 +116,14 @@ template <int DT, bool SUM>
 __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict__ x, ColArgs a) {
   pdl_entry();
   // stage A reduction buffer; the last CTA reuses it for S and the stats scratch
-  __shared__ __align__(16) unsigned char s_buf[kTailSmem];
-  static_assert(kTailSmem >= kRowLanes * 32 * 8 * sizeof(double), "stage A buffer");
+  extern __shared__ __align__(16) unsigned char s_buf[];  // col_smem(SUM, cols) bytes
   double(*red)[32][8] = reinterpret_cast<double(*)[32][8]>(s_buf);
   __shared__ int s_last;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int64_t cols = a.cols, rows = a.rows;
   const int64_t cu = static_cast<int64_t>(blockIdx.x) * 32 + tx;
   const bool live = cu * 8 < cols;
+  CR_TRACE(0);
 
   // ---- stage A: this CTA's rows, 8 columns per thread, 8 loads in flight
   double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -137,6 +165,7 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
       }
     }
   }
+  CR_TRACE(1);
   if (SUM) {
 #pragma unroll
     for (int j = 0; j < 8; ++j) red[ty][tx][j] = acc[j];
@@ -173,21 +202,23 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
   if (threadIdx.x == 0)
     s_last = atom_add_acq_rel_gpu(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
+  CR_TRACE(2);
   if (!s_last) return;
-  // move the accumulators out (4 columns per thread per round trip) and reset them
+  CR_TRACE_TAIL(0);
+  // move the accumulators out (8 columns per thread per round trip) and reset them
   const bool s_smem = SUM && cols <= kSmemSumCols;
   double *s_S = reinterpret_cast<double *>(s_buf);
   int flagged = 0;
-  for (int64_t base = 0; base < cols; base += 4 * kThreads) {
+  for (int64_t base = 0; base < cols; base += 8 * kThreads) {
     if (SUM) {
-      double v[4];
+      double v[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
         v[q] = c < cols ? __ldcg(a.acc + c) : 0.0;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
         if (c < cols) {
           __stcg(a.acc + c, 0.0);
@@ -197,14 +228,14 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
         }
       }
     } else {
-      uint32_t m[4];
+      uint32_t m[8];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
         m[q] = c < cols ? __ldcg(a.macc + c) : 0u;
       }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
+      for (int q = 0; q < 8; ++q) {
         const int64_t c = base + q * kThreads + threadIdx.x;
         if (c < cols) {
           __stcg(a.macc + c, 0u);
@@ -216,6 +247,7 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
   }
   if (threadIdx.x == 0) a.done_cnt[0] = 0;  // reset for the next call
   flagged = __syncthreads_or(flagged);
+  CR_TRACE_TAIL(1);
   if (!SUM) {
     if (flagged && threadIdx.x == 0 && a.err) atomicOr(a.err, ADC_ERR_NONFINITE);
     return;
@@ -230,11 +262,14 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
   if (a.do_stats) {
     if (s_smem)
       outlier_stats_block<true>(s_S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
-                                a.err, a.too_many_check != 0, s_buf + kSmemSumCols * 8);
+                                a.err, a.too_many_check != 0, s_buf + ((cols * 8 + 15) & ~int64_t{15}),
+                                a.trace ? g_crtrace + kCrTraceCtas * 4 + 4 : nullptr);
     else
       outlier_stats_block<false>(a.S, rows, cols, a.thr, a.k_cap, a.tree, a.flag, a.idx, a.k_out,
-                                 a.err, a.too_many_check != 0, s_buf);
+                                 a.err, a.too_many_check != 0, s_buf,
+                                 a.trace ? g_crtrace + kCrTraceCtas * 4 + 4 : nullptr);
   }
+  CR_TRACE_TAIL(2);
 }
 
 // ---------------------------------------------------------------------------
@@ -283,8 +318,16 @@ __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restr
     default: return -1;                                              \
   }
 
+static std::atomic<int> g_cr_trace{0};
+void set_cr_trace(int v) { g_cr_trace.store(v, std::memory_order_relaxed); }
+int read_cr_trace(unsigned long long *host, int n) {
+  n = n < kCrTraceCtas * 4 + 16 ? n : kCrTraceCtas * 4 + 16;
+  return cudaMemcpyFromSymbol(host, g_crtrace, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
+}
+
 static ColArgs make_args(int64_t rows, int64_t cols, const Workspace &ws) {
   ColArgs a{};
+  a.trace = g_cr_trace.load(std::memory_order_relaxed);
   a.rows = rows;
   a.cols = cols;
   a.acc = ws.acc;
@@ -304,12 +347,30 @@ static bool fast_cols(const void *x, int64_t cols) {
 // One full wave: column strips x row blocks ~= SMs x resident CTAs per SM,
 // at least one row per row lane.
 template <typename K>
-static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols) {
-  static int occ = 0;
-  if (occ == 0) {
-    int v = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, kThreads, 0);
-    occ = v > 0 ? v : 1;
+static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols, int smem) {
+  // occupancy per (kernel, dynamic shared-memory size); every instantiation
+  // shares this function's type, so the cache is keyed by the kernel pointer
+  struct Entry { const void *k; int smem, occ; };
+  static Entry cache[32];
+  static int used = 0;
+  static std::mutex mu;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    bool seen = false;
+    for (int i = 0; i < used; ++i) {
+      if (cache[i].k != reinterpret_cast<const void *>(kernel)) continue;
+      seen = true;
+      if (cache[i].smem == smem) occ = cache[i].occ;
+    }
+    if (!seen)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem(true, kSmemSumCols));
+    if (occ == 0) {
+      int v = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, kThreads, smem);
+      occ = v > 0 ? v : 1;
+      if (used < 32) cache[used++] = Entry{reinterpret_cast<const void *>(kernel), smem, occ};
+    }
   }
   const int64_t gx = (cols + kStripCols - 1) / kStripCols;
   int64_t gy = static_cast<int64_t>(c.num_sms) * occ / gx;  // never a partial second wave
@@ -333,8 +394,9 @@ int launch_colstats_sum(const Ctx &c, const void *x, int dt, int64_t rows, int64
   a.err = err;
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
-      const dim3 g = col_grid(c, colreduce<DT, true>, rows, cols);
-      launch_k(colreduce<DT, true>, g, kThreads, 0, c.stream, x, a);
+      const int smem = col_smem(true, cols);
+      const dim3 g = col_grid(c, colreduce<DT, true>, rows, cols, smem);
+      launch_k(colreduce<DT, true>, g, kThreads, smem, c.stream, x, a);
       note_launches(1);
     });
   } else {
@@ -350,8 +412,9 @@ int launch_colstats_max(const Ctx &c, const void *x, int dt, int64_t rows, int64
   a.err = err;
   if (fast_cols(x, cols)) {
     ADC_DT_SWITCH(dt, DT, {
-      const dim3 g = col_grid(c, colreduce<DT, false>, rows, cols);
-      launch_k(colreduce<DT, false>, g, kThreads, 0, c.stream, x, a);
+      const int smem = col_smem(false, cols);
+      const dim3 g = col_grid(c, colreduce<DT, false>, rows, cols, smem);
+      launch_k(colreduce<DT, false>, g, kThreads, smem, c.stream, x, a);
       note_launches(1);
     });
   } else {
