@@ -45,7 +45,7 @@ import torch
 
 from . import codec as C
 from .profiles import LayerKind
-from .slots import CodecSlot
+from .slots import CodecSlot, Int8Slot
 
 RETAIN, COMPRESS, RECOMPUTE = "retain", "compress", "recompute"
 
@@ -79,8 +79,12 @@ class Stats:
 
 class ActivationPolicy:
     def __init__(self, ops: list[OpInfo], plan: dict[int, str] | None = None,
-                 min_numel: int = 1 << 15, k_caps: dict[int, int] | None = None):
+                 min_numel: int = 1 << 15, k_caps: dict[int, int] | None = None,
+                 codec_overrides: dict[LayerKind, str] | None = None):
         self.ops = {o.op_id: o for o in ops}
+        # kinds compressed with the int8 / float32-scale EXTENSION codec ("int8")
+        # instead of the reference's scheme_for(kind) (not reference behaviour)
+        self.codec_overrides = dict(codec_overrides or {})
         self.plan = dict(plan or {})
         self.min_numel = min_numel
         self.k_caps = dict(k_caps or {})
@@ -207,7 +211,16 @@ class ActivationPolicy:
             self.stats.original_bytes += nbytes
             return _Base(RECOMPUTE, None, (fn, packed_inputs), tuple(base.shape), base.dtype,
                          weakref.ref(base))
-        spec = C.scheme_for(self.ops[op_id].kind)
+        kind = self.ops[op_id].kind
+        if self.codec_overrides.get(kind) == "int8" and base.dtype in (torch.bfloat16, torch.float16, torch.float32):
+            x = base.reshape(-1, base.shape[-1])
+            slot = self._slot_int8(op_id, x)
+            slot.compress_ptr(x.data_ptr(), torch.cuda.current_stream(x.device).cuda_stream)
+            self.stats.compressed += 1
+            self.stats.original_bytes += nbytes
+            self.stats.stored_bytes += slot.device_bytes
+            return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base))
+        spec = C.scheme_for(kind)
         if spec.scheme is C.Scheme.BIT_MASK:
             if base.dtype not in (torch.bool, torch.uint8):
                 return None
@@ -237,6 +250,16 @@ class ActivationPolicy:
             out_dt = torch.uint8 if spec.scheme is C.Scheme.BIT_MASK else x.dtype
             slot = CodecSlot(x.shape[0], x.shape[1], spec, in_dt, out_dt, k_cap=k_cap, device=x.device,
                              status=self.status)
+            self._pool[(sig, n)] = slot
+        return slot
+
+    def _slot_int8(self, op_id, x) -> Int8Slot:
+        sig = (op_id, "int8", tuple(x.shape), x.dtype)
+        n = self._occ.get(sig, 0)
+        self._occ[sig] = n + 1
+        slot = self._pool.get((sig, n))
+        if slot is None:
+            slot = Int8Slot(x.shape[0], x.shape[1], 128, x.dtype, x.dtype, device=x.device, status=self.status)
             self._pool[(sig, n)] = slot
         return slot
 

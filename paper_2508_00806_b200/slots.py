@@ -125,3 +125,44 @@ class CodecSlot:
                                 outlier_indices=self.idx, outlier_values=self.val,
                                 mask_bits=self.codes if self.scheme is Scheme.BIT_MASK else None,
                                 k_dev=self.k_status, k_cap=self.k_cap)
+
+
+class Int8Slot:
+    """Preallocated int8 group codes + float32 scales (the EXTENSION codec,
+    ``adc_compress_int8``; no reference counterpart): the same launch-path
+    interface as :class:`CodecSlot`, for kinds a caller moves to 8-bit codes
+    (``ActivationPolicy(codec_overrides=...)``)."""
+
+    k_cap = 0
+
+    def __init__(self, rows: int, cols: int, group: int, in_dtype: torch.dtype,
+                 out_dtype: torch.dtype | None = None, *, device=None, status: torch.Tensor | None = None):
+        self.rows, self.cols, self.group = int(rows), int(cols), int(group)
+        self.in_dtype = in_dtype
+        self.out_dtype = out_dtype or in_dtype
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.device = dev
+        n = self.rows * self.cols
+        self.codes = torch.empty(n, dtype=torch.int8, device=dev)
+        self.scales = torch.empty(-(-n // self.group), dtype=torch.float32, device=dev)
+        self.status = status if status is not None else torch.zeros(2, dtype=torch.int32, device=dev)
+        self._compress = _lib.lib().adc_compress_int8
+        self._decompress = _lib.lib().adc_decompress_int8
+        self._c = (_IN[in_dtype], self.rows, self.cols, self.group, self.codes.data_ptr(),
+                   self.scales.data_ptr(), self.status.data_ptr())
+        self._d = (self.codes.data_ptr(), self.scales.data_ptr(), self.rows, self.cols, self.group)
+        self._out_code = _IN[self.out_dtype]
+
+    def compress_ptr(self, x_ptr: int, stream: int) -> None:
+        st = self._compress(x_ptr, *self._c, stream)
+        if st:
+            _lib.check(st, "compress_int8")
+
+    def decompress_ptr(self, y_ptr: int, stream: int) -> None:
+        st = self._decompress(*self._d, y_ptr, self._out_code, stream)
+        if st:
+            _lib.check(st, "decompress_int8")
+
+    @property
+    def device_bytes(self) -> int:
+        return self.codes.numel() + 4 * self.scales.numel()

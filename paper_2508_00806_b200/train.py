@@ -86,8 +86,9 @@ def plan_for(strategy: str, prof=None) -> dict:
 
 class Trainer:
     def __init__(self, cfg: GPTConfig, batch: int, *, lr: float = 3e-4, rank: int = 0,
-                 world: int = 1, device=None, ddp: bool = False):
+                 world: int = 1, device=None, ddp: bool = False, lr_warmup: int = 0):
         self.cfg, self.batch, self.rank, self.world = cfg, batch, rank, world
+        self.lr, self.lr_warmup = lr, int(lr_warmup)
         self.device = device or torch.device("cuda", torch.cuda.current_device())
         torch.manual_seed(1234)
         model = GPT(cfg).to(self.device, dtype=torch.bfloat16)
@@ -113,6 +114,10 @@ class Trainer:
     def step(self, idx, tgt) -> torch.Tensor:
         loss = self._forward(idx, tgt, self.pol)
         loss.backward()
+        if self.lr_warmup:  # linear warm-up over the first lr_warmup steps of a run
+            lr = self.lr * min(1.0, (self.step_id + 1) / self.lr_warmup)
+            for g in self.opt.param_groups:
+                g["lr"] = lr
         self.opt.step()
         self.opt.zero_grad(set_to_none=True)
         self.step_id += 1
@@ -184,6 +189,12 @@ def _calibrate(tr, prof, cap, snap_model, snap_opt, dev, world, rounds: int = 6)
     return plan, log
 
 
+def _overrides(kinds: str) -> dict:
+    """--int8-kinds softmax,score -> {LayerKind.SOFTMAX: "int8", ...} (EXTENSION codec)."""
+    from .profiles import LayerKind
+    return {LayerKind(k.strip()): "int8" for k in (kinds or "").split(",") if k.strip()}
+
+
 def run(args) -> dict:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -194,7 +205,9 @@ def run(args) -> dict:
         dist.init_process_group("nccl", device_id=dev)
     cfg = GPTConfig.named(args.model)
     cfg.seq = args.seq or cfg.seq
-    tr = Trainer(cfg, args.batch, rank=rank, world=world, device=dev, ddp=world > 1)
+    tr = Trainer(cfg, args.batch, rank=rank, world=world, device=dev, ddp=world > 1,
+                 lr_warmup=getattr(args, "lr_warmup", 0))
+    tr.pol.codec_overrides = _overrides(getattr(args, "int8_kinds", ""))
     total_hbm = torch.cuda.get_device_properties(dev).total_memory
     cap = int(args.mem_cap_gb * (1 << 30)) if args.mem_cap_gb else total_hbm
     # warm-up with retain-all to size static memory and the base step time
@@ -208,7 +221,8 @@ def run(args) -> dict:
     torch.cuda.synchronize()
     base_ms = (time.perf_counter() - t0) * 1e3
     out = {"model": args.model, "params": tr.model.n_params(), "batch_per_gpu": args.batch,
-           "seq": cfg.seq, "n_gpus": world, "mem_cap_bytes": cap, "results": {}}
+           "seq": cfg.seq, "n_gpus": world, "mem_cap_bytes": cap, "lr": tr.lr, "lr_warmup": tr.lr_warmup,
+           "int8_kinds": sorted(k.value for k in tr.pol.codec_overrides), "results": {}}
     prof = None
     if "adacc" in args.policy or args.profile_out:
         prof, k_caps = tr.profile(cap, base_ms)
@@ -380,6 +394,9 @@ def main(argv=None):
     ap.add_argument("--profile-out", default="")
     ap.add_argument("--codec-share", action="store_true", help="profile one step: codec kernels' share of device time")
     ap.add_argument("--loss-curve", action="store_true", help="include a subsampled loss curve per strategy")
+    ap.add_argument("--lr-warmup", type=int, default=0, help="linear learning-rate warm-up steps")
+    ap.add_argument("--int8-kinds", default="",
+                    help="layer kinds compressed with the int8 / f32-scale EXTENSION codec (e.g. softmax)")
     ap.add_argument("--evolve", type=int, default=0, help="config 5: N iterations of policy evolution")
     ap.add_argument("--max-interval", type=int, default=64)
     ap.add_argument("--settle", type=int, default=150)

@@ -167,3 +167,35 @@ def test_profiler_times_the_real_qkv_projection(tiny):
     gemm_ms_floor = 2 * tokens * d * 3 * d / 2.25e15 * 1e3  # 2.25 PFLOP/s dense bf16 spec
     assert ops["qkv"]["compute_time_ms"] >= gemm_ms_floor, ops["qkv"]
     assert ops["mlp_up"]["compute_time_ms"] >= 2 * tokens * d * 4 * d / 2.25e15 * 1e3
+
+
+def test_int8_codec_override_for_softmax(tiny):
+    """codec_overrides moves a kind to the int8 / float32-scale EXTENSION codec
+    (pooled Int8Slots): forward unchanged, gradients closer to retain-all than
+    the reference's int4 softmax codec."""
+    import torch
+    from paper_2508_00806_b200.gpt import BLOCK_OPS, GPT, synthetic_batch
+    from paper_2508_00806_b200.hooks import ActivationPolicy
+    from paper_2508_00806_b200.profiles import LayerKind
+    from paper_2508_00806_b200.slots import Int8Slot
+    from paper_2508_00806_b200.train import plan_for
+
+    def grads(plan, overrides=None):
+        torch.manual_seed(0)
+        model = GPT(tiny).cuda().to(torch.bfloat16)
+        pol = ActivationPolicy(BLOCK_OPS, plan_for(plan), min_numel=1024, codec_overrides=overrides)
+        idx, tgt = synthetic_batch(0, 0, 4, tiny.seq, tiny.vocab, "cuda")
+        loss = model(idx, tgt, pol, seed=3)
+        loss.backward()
+        g = torch.cat([p.grad.float().flatten() for n, p in model.named_parameters()
+                       if not n.startswith(("wte", "wpe"))])
+        return loss.item(), g, pol
+
+    l0, g0, _ = grads("retain-all")
+    l4, g4, _ = grads("all-compress")
+    l8, g8, pol8 = grads("all-compress", {LayerKind.SOFTMAX: "int8", LayerKind.SCORE: "int8"})
+    assert l0 == l4 == l8
+    assert any(isinstance(s, Int8Slot) for s in pol8._pool.values())
+    cos = torch.nn.functional.cosine_similarity
+    assert cos(g0, g8, dim=0).item() >= cos(g0, g4, dim=0).item() - 1e-4
+    assert pol8.check() == 0
