@@ -333,7 +333,7 @@ def evolve(args) -> dict:
     snap_opt = _clone_state(tr.opt.state_dict())
     ids = [o.op_id for o in BLOCK_OPS]
     out = {"model": args.model, "iterations": n, "mem_cap_bytes": cap, "max_interval": args.max_interval,
-           "drift_counts": [int(c) for c in counts[:: max(1, n // 32)]], "arms": {}}
+           "drift_counts": [int(c) for c in counts[:: max(1, n // 32)]], "profile": prof0.to_dict(), "arms": {}}
     for arm in ("static", "adaptive"):
         tr.model.load_state_dict(snap_model)
         tr.opt.load_state_dict(_clone_state(snap_opt))
