@@ -60,12 +60,13 @@ class OpInfo:
 class _Base:
     """One packed base storage (compressed or recompute recipe), shared by views."""
 
-    __slots__ = ("kind", "slot", "recipe", "shape", "dtype", "value", "src", "__weakref__")
+    __slots__ = ("kind", "slot", "recipe", "shape", "dtype", "value", "src", "ready", "__weakref__")
 
-    def __init__(self, kind, slot, recipe, shape, dtype, src):
+    def __init__(self, kind, slot, recipe, shape, dtype, src, ready=None):
         self.kind, self.slot, self.recipe, self.shape, self.dtype = kind, slot, recipe, shape, dtype
         self.value = None
         self.src = src  # weakref to the packed base tensor: detects address reuse
+        self.ready = ready  # event after the compress when it ran on the codec stream
 
 
 @dataclass
@@ -85,6 +86,10 @@ class ActivationPolicy:
         # kinds compressed with the int8 / float32-scale EXTENSION codec ("int8")
         # instead of the reference's scheme_for(kind) (not reference behaviour)
         self.codec_overrides = dict(codec_overrides or {})
+        # optional side stream for the forward's compress calls: they start
+        # when their activation is produced and overlap the next forward ops;
+        # the backward's decompress waits for the compress's event
+        self.codec_stream: torch.cuda.Stream | None = None
         self.plan = dict(plan or {})
         self.min_numel = min_numel
         self.k_caps = dict(k_caps or {})
@@ -215,11 +220,11 @@ class ActivationPolicy:
         if self.codec_overrides.get(kind) == "int8" and base.dtype in (torch.bfloat16, torch.float16, torch.float32):
             x = base.reshape(-1, base.shape[-1])
             slot = self._slot_int8(op_id, x)
-            slot.compress_ptr(x.data_ptr(), torch.cuda.current_stream(x.device).cuda_stream)
+            ready = self._launch_compress(slot, x)
             self.stats.compressed += 1
             self.stats.original_bytes += nbytes
             self.stats.stored_bytes += slot.device_bytes
-            return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base))
+            return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base), ready)
         spec = C.scheme_for(kind)
         if spec.scheme is C.Scheme.BIT_MASK:
             if base.dtype not in (torch.bool, torch.uint8):
@@ -231,12 +236,28 @@ class ActivationPolicy:
         if spec.scheme is C.Scheme.OUTLIER_SEPARATED:
             k_cap = self.k_caps.get(op_id, max(16, x.shape[1] // 32))
         slot = self._slot(op_id, spec, x, k_cap)
-        slot.compress_ptr(x.data_ptr(), torch.cuda.current_stream(x.device).cuda_stream)
+        ready = self._launch_compress(slot, x)
         self.stats.compressed += 1
         self.stats.original_bytes += nbytes
         self.stats.stored_bytes += slot.device_bytes
         self.records.setdefault(op_id, []).append(slot)
-        return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base))
+        return _Base(COMPRESS, slot, None, tuple(base.shape), base.dtype, weakref.ref(base), ready)
+
+    def _launch_compress(self, slot, x):
+        """Compress on the current stream, or on the codec stream after the
+        producer (x is kept alive for that stream); returns the event the
+        backward's decompress waits for (None on the current stream)."""
+        cur = torch.cuda.current_stream(x.device)
+        cs = self.codec_stream
+        if cs is None:
+            slot.compress_ptr(x.data_ptr(), cur.cuda_stream)
+            return None
+        cs.wait_stream(cur)
+        slot.compress_ptr(x.data_ptr(), cs.cuda_stream)
+        x.record_stream(cs)
+        ev = torch.cuda.Event()
+        ev.record(cs)
+        return ev
 
     def _slot(self, op_id, spec, x, k_cap) -> CodecSlot:
         """The pooled slot of this (operator, shape, dtype, capacity)'s n-th
@@ -276,6 +297,8 @@ class ActivationPolicy:
         else:
             slot = entry.slot
             out = torch.empty((slot.rows, slot.cols), dtype=slot.out_dtype, device=slot.device)
+            if entry.ready is not None:
+                torch.cuda.current_stream(out.device).wait_event(entry.ready)
             slot.decompress_ptr(out.data_ptr(), torch.cuda.current_stream(out.device).cuda_stream)
             if entry.dtype == torch.bool:
                 out = out.view(torch.bool)
@@ -297,6 +320,8 @@ class ActivationPolicy:
         """Device error word accumulated since the last check (synchronises)."""
         if self.status is None:
             return 0
+        if self.codec_stream is not None:
+            self.codec_stream.synchronize()
         err = int(self.status[0].item()) & 0xffffffff
         self.status.zero_()
         return err

@@ -208,6 +208,8 @@ def run(args) -> dict:
     tr = Trainer(cfg, args.batch, rank=rank, world=world, device=dev, ddp=world > 1,
                  lr_warmup=getattr(args, "lr_warmup", 0))
     tr.pol.codec_overrides = _overrides(getattr(args, "int8_kinds", ""))
+    if getattr(args, "codec_stream", False):
+        tr.pol.codec_stream = torch.cuda.Stream(dev)
     total_hbm = torch.cuda.get_device_properties(dev).total_memory
     cap = int(args.mem_cap_gb * (1 << 30)) if args.mem_cap_gb else total_hbm
     # warm-up with retain-all to size static memory and the base step time
@@ -222,7 +224,8 @@ def run(args) -> dict:
     base_ms = (time.perf_counter() - t0) * 1e3
     out = {"model": args.model, "params": tr.model.n_params(), "batch_per_gpu": args.batch,
            "seq": cfg.seq, "n_gpus": world, "mem_cap_bytes": cap, "lr": tr.lr, "lr_warmup": tr.lr_warmup,
-           "int8_kinds": sorted(k.value for k in tr.pol.codec_overrides), "results": {}}
+           "int8_kinds": sorted(k.value for k in tr.pol.codec_overrides),
+           "codec_stream": tr.pol.codec_stream is not None, "results": {}}
     prof = None
     if "adacc" in args.policy or args.profile_out:
         prof, k_caps = tr.profile(cap, base_ms)
@@ -397,6 +400,8 @@ def main(argv=None):
     ap.add_argument("--lr-warmup", type=int, default=0, help="linear learning-rate warm-up steps")
     ap.add_argument("--int8-kinds", default="",
                     help="layer kinds compressed with the int8 / f32-scale EXTENSION codec (e.g. softmax)")
+    ap.add_argument("--codec-stream", action="store_true",
+                    help="compress on a side stream overlapping the forward (decompress waits on its event)")
     ap.add_argument("--evolve", type=int, default=0, help="config 5: N iterations of policy evolution")
     ap.add_argument("--max-interval", type=int, default=64)
     ap.add_argument("--settle", type=int, default=150)

@@ -199,3 +199,33 @@ def test_int8_codec_override_for_softmax(tiny):
     cos = torch.nn.functional.cosine_similarity
     assert cos(g0, g8, dim=0).item() >= cos(g0, g4, dim=0).item() - 1e-4
     assert pol8.check() == 0
+
+
+def test_codec_stream_overlap_is_exact(tiny):
+    """Compressing on a side stream (codec_stream) overlaps the forward and
+    gives bit-identical gradients to compressing on the compute stream."""
+    import torch
+    from paper_2508_00806_b200.gpt import BLOCK_OPS, GPT, synthetic_batch
+    from paper_2508_00806_b200.hooks import ActivationPolicy
+    from paper_2508_00806_b200.train import plan_for
+
+    def grads(side):
+        torch.manual_seed(0)
+        model = GPT(tiny).cuda().to(torch.bfloat16)
+        pol = ActivationPolicy(BLOCK_OPS, plan_for("all-compress"), min_numel=1024)
+        if side:
+            pol.codec_stream = torch.cuda.Stream()
+        idx, tgt = synthetic_batch(0, 0, 4, tiny.seq, tiny.vocab, "cuda")
+        for _ in range(2):  # the second step reuses the pooled slots across streams
+            model.zero_grad(set_to_none=True)
+            loss = model(idx, tgt, pol, seed=3)
+            loss.backward()
+        g = torch.cat([p.grad.float().flatten() for n, p in model.named_parameters()
+                       if not n.startswith(("wte", "wpe"))])
+        assert pol.check() == 0
+        return loss.item(), g
+
+    l0, g0 = grads(False)
+    l1, g1 = grads(True)
+    assert l0 == l1
+    assert torch.equal(g0, g1)
