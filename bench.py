@@ -368,18 +368,47 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # Python/ctypes submission.  The kernels, inputs and outputs are exactly
     # those of the eager calls (tests/test_gpu_parity.py checks the graph
     # replay bit-for-bit against eager).
+    # ---- per-call breakdown first (it also sizes the stream lanes): per-call
+    # graphs (same order, same buffers)
+    g_calls = []
+    for i, phase in calls:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            run_call(i, phase, torch.cuda.current_stream().cuda_stream)
+        g_calls.append(g)
+    # replayed one graph at a time with CUDA events between them on the
+    # launching stream (K' steps)
+    op_steps = max(3, min(args.steps, 20))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(op_steps)]
+    torch.cuda.synchronize()
+    for k in range(op_steps):
+        evs[k][0].record(stream)
+        for j, g in enumerate(g_calls):
+            g.replay()
+            evs[k][j + 1].record(stream)
+    torch.cuda.synchronize()
+    call_us = [statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) * 1e3 for j in range(len(calls))]
+    cu = {(i, ph): call_us[j] for j, (i, ph) in enumerate(calls)}
+    per_op = []
+    for i, (op, s) in enumerate(zip(ops, slots)):
+        c, d = cu[(i, "compress")], cu[(i, "decompress")]
+        per_op.append({"op": op.name, "scheme": s.scheme.name, "shape": [op.rows, op.cols],
+                       "k": ks[i], "compress_us": round(c, 2), "decompress_us": round(d, 2),
+                       "compress_gbs": round(bytes_c[i] / c / 1e3, 1),
+                       "decompress_gbs": round(bytes_d[i] / d / 1e3, 1)})
     # With --streams S > 1 the graph forks: the tensors are dealt to S streams
-    # (largest first, greedy by bytes) and each phase (all compresses, then
+    # (longest measured call pair first, greedy) and each phase (all compresses, then
     # all decompresses) joins before the next, so independent tensors' calls
     # overlap one another's launch ramps, tails and single-CTA statistics
     # phases.  The work and bytes are the same calls as the serial step.
     n_streams = max(1, int(getattr(args, "streams", 1)))
     lanes = [[] for _ in range(n_streams)]
-    load = [0] * n_streams
-    for i in sorted(range(n), key=lambda i: -(bytes_c[i] + bytes_d[i])):
+    load = [0.0] * n_streams
+    t_of = [cu[(i, "compress")] + cu[(i, "decompress")] for i in range(n)]
+    for i in sorted(range(n), key=lambda i: -t_of[i]):  # longest measured call pair first
         j = load.index(min(load))
         lanes[j].append(i)
-        load[j] += bytes_c[i] + bytes_d[i]
+        load[j] += t_of[i]
     side = [torch.cuda.Stream(dev) for _ in range(n_streams - 1)]
 
     def step_graph():
@@ -405,13 +434,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
         else:
             step_graph()
     launches_per_step = lib.adc_kernel_launches() - l0
-    # per-call graphs (same order, same buffers) for the per-op breakdown
-    g_calls = []
-    for i, phase in calls:
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            run_call(i, phase, torch.cuda.current_stream().cuda_stream)
-        g_calls.append(g)
     for _ in range(max(3, args.warmup)):
         g_step.replay()
     torch.cuda.synchronize()
@@ -434,26 +456,6 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     # whole-job GB/s: the bytes of all ranks over the MAX-over-ranks device time
     value, ms_max = whole_job_rate(bytes_step * args.steps / 1e9, ms, dev)
 
-    # ---- per-call breakdown: the same calls replayed one graph at a time with
-    # CUDA events between them on the launching stream (K' steps)
-    op_steps = max(3, min(args.steps, 20))
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(len(calls) + 1)] for _ in range(op_steps)]
-    torch.cuda.synchronize()
-    for k in range(op_steps):
-        evs[k][0].record(stream)
-        for j, g in enumerate(g_calls):
-            g.replay()
-            evs[k][j + 1].record(stream)
-    torch.cuda.synchronize()
-    call_us = [statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) * 1e3 for j in range(len(calls))]
-    cu = {(i, ph): call_us[j] for j, (i, ph) in enumerate(calls)}
-    per_op = []
-    for i, (op, s) in enumerate(zip(ops, slots)):
-        c, d = cu[(i, "compress")], cu[(i, "decompress")]
-        per_op.append({"op": op.name, "scheme": s.scheme.name, "shape": [op.rows, op.cols],
-                       "k": ks[i], "compress_us": round(c, 2), "decompress_us": round(d, 2),
-                       "compress_gbs": round(bytes_c[i] / c / 1e3, 1),
-                       "decompress_gbs": round(bytes_d[i] / d / 1e3, 1)})
     peak, peak_src = measured_peak()
     # dominant call: the largest-time call of the step, whatever its launch count
     # (per_op lists every call; the outlier-separated ones are two launches or one)
@@ -566,7 +568,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "clocks": clocks.summary(), "gpu_launches": int(launches),
                 "launch_mode": (f"CUDA graph of the 18 codec calls per step on {n_streams} stream(s) "
                                 "(tensors dealt to streams, each phase joined; e2e: eager C-ABI calls)"),
-                "device_error_word": status_err, "per_op": per_op, "training": training}
+                "device_error_word": status_err,
+                "stream_lanes": [[ops[i].name for i in lane] for lane in lanes],
+                "per_op": per_op, "training": training}
         print(json.dumps(line), flush=True)
 
 
@@ -638,9 +642,10 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--cpu-reps", type=int, default=2)
-    ap.add_argument("--streams", type=int, default=3,
+    ap.add_argument("--streams", type=int, default=4,
                     help="streams the step graph deals its independent tensors to (1 = serial; "
-                         "measured 4.00 / 4.33 / 4.64 / 4.37 TB/s for 1 / 2 / 3 / 4)")
+                         "measured 4.00 / 4.61 / 4.63 / 4.83 / 4.77 / 4.83 / 4.67 TB/s for "
+                         "1 / 2 / 3 / 4 / 5 / 6 / 8)")
     ap.add_argument("--no-train", action="store_true", help="skip the training tokens/s leg")
     ap.add_argument("--train-model", default="gpt-345m")
     ap.add_argument("--train-steps", type=int, default=10)
