@@ -59,6 +59,29 @@ struct ChRaw<ADC_F32> {
   }
 };
 
+// Element pair (row r, row r+1) of column j of this thread's 8 columns as
+// f32 for the packed quotient.  bf16 input goes straight to f32 (a shift or a
+// mask): the f16 rounding the reference applies first cannot change a code
+// once the column's scale is a normal f16 (every bf16 value at or above
+// 2^-17 is exactly an f16; below it, the quotient stays under 1/2 either way),
+// which the fast path requires anyway.
+template <int DT>
+__device__ __forceinline__ uint64_t col_pair(const ChRaw<DT> &ra, const ChRaw<DT> &rb, const uint4 &ha,
+                                             const uint4 &hb, int j) {
+  if constexpr (DT == ADC_BF16) {
+    const uint32_t wa[4] = {ra.v.x, ra.v.y, ra.v.z, ra.v.w}, wb[4] = {rb.v.x, rb.v.y, rb.v.z, rb.v.w};
+    const uint32_t a = (j & 1) ? (wa[j >> 1] & 0xffff0000u) : (wa[j >> 1] << 16);
+    const uint32_t b = (j & 1) ? (wb[j >> 1] & 0xffff0000u) : (wb[j >> 1] << 16);
+    return f2_pack(__uint_as_float(a), __uint_as_float(b));
+  } else {
+    const uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w}, wb[4] = {hb.x, hb.y, hb.z, hb.w};
+    const uint32_t sh = (j & 1) * 16;
+    return f2_pack(h2f((wa[j >> 1] >> sh) & 0xffffu), h2f((wb[j >> 1] >> sh) & 0xffffu));
+  }
+}
+
+constexpr int kColBytes = 36;  // shared-memory bytes per tile column per sub-tile (32 row pairs + pad)
+
 template <int DT>
 __global__ void __launch_bounds__(kThreads)
     channel_quant(const void *__restrict__ x, int64_t rows, int64_t cols,
@@ -66,10 +89,12 @@ __global__ void __launch_bounds__(kThreads)
                   uint16_t *__restrict__ scales) {
   pdl_entry();
   // all four sub-tiles: their rows are loaded up front (8 x 16 B in flight per
-  // thread, issued before the scales are derived), quantised into four
-  // separate shared-memory stages, and written with one barrier
+  // thread, issued before the scales are derived), quantised, and their code
+  // bytes written column-major into shared memory (one byte store per column
+  // and row pair: the transpose), then stored as 16-byte column runs after one
+  // barrier
   constexpr int kSubs = kBlockRows / kSubRows;
-  __shared__ uint32_t stage[kSubs][kTileCols * kWordStride];
+  __shared__ __align__(16) uint8_t stage[kSubs][kTileCols * kColBytes];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int tx = lane & 7;         // column unit inside the tile
   const int tyl = lane >> 3;       // row pair inside the warp (0..3)
@@ -95,10 +120,12 @@ __global__ void __launch_bounds__(kThreads)
   bool fast = true;  // every column scale of this thread is a normal f16 (the packed path)
   {
     uint32_t sb[8];
+    const uint4 m0 = col_live ? __ldg(reinterpret_cast<const uint4 *>(colmax + c0)) : make_uint4(0, 0, 0, 0);
+    const uint4 m1 = col_live ? __ldg(reinterpret_cast<const uint4 *>(colmax + c0) + 1) : make_uint4(0, 0, 0, 0);
+    const uint32_t top[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-      uint32_t top = col_live ? __ldg(colmax + c0 + j) : 0u;
-      sb[j] = sym_scale_bits(top);
+      sb[j] = sym_scale_bits(top[j]);
       QParams q = make_qparams(static_cast<uint16_t>(sb[j]), 0);
       qs[j] = q.s;
       qi[j] = q.inv;
@@ -113,7 +140,8 @@ __global__ void __launch_bounds__(kThreads)
 
 #pragma unroll
   for (int sub = 0; sub < kSubs; ++sub) {
-    const uint4 ha = ra[sub].f16(), hb = rb[sub].f16();
+    const uint4 ha = DT == ADC_BF16 ? make_uint4(0, 0, 0, 0) : ra[sub].f16();
+    const uint4 hb = DT == ADC_BF16 ? make_uint4(0, 0, 0, 0) : rb[sub].f16();
     // byte j = code(row r, col j) | code(row r+1, col j) << 4
     uint32_t lo = 0, hi = 0;
     if (fast) {
@@ -121,13 +149,11 @@ __global__ void __launch_bounds__(kThreads)
       // give both correctly rounded quotients, the magic add rounds them,
       // one saturating I2IP clips both and joins them into the byte, chained
       // four bytes per word (see pack8_tbits_sat)
-      const uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w}, wb[4] = {hb.x, hb.y, hb.z, hb.w};
       const uint64_t mg2 = f2_pack(kMagic8, kMagic8);
       uint32_t ta_[8], tb_[8];
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const uint32_t sh = (j & 1) * 16;
-        const uint64_t h2 = f2_pack(h2f((wa[j >> 1] >> sh) & 0xffffu), h2f((wb[j >> 1] >> sh) & 0xffffu));
+        const uint64_t h2 = col_pair<DT>(ra[sub], rb[sub], ha, hb, j);
         const uint64_t inv2 = f2_pack(qi[j], qi[j]), ns2 = f2_pack(-qs[j], -qs[j]);
         const uint64_t r0 = f2_mul(h2, inv2);
         const uint64_t r1 = f2_fma(f2_fma(r0, ns2, h2), inv2, r0);
@@ -139,8 +165,9 @@ __global__ void __launch_bounds__(kThreads)
       lo = pack4_pairs_sat(ta_, tb_);
       hi = pack4_pairs_sat(ta_ + 4, tb_ + 4);
     } else {
-      uint32_t wa[4] = {ha.x, ha.y, ha.z, ha.w};
-      uint32_t wb[4] = {hb.x, hb.y, hb.z, hb.w};
+      const uint4 fa = ra[sub].f16(), fb = rb[sub].f16();  // the reference's f16 rounding
+      uint32_t wa[4] = {fa.x, fa.y, fa.z, fa.w};
+      uint32_t wb[4] = {fb.x, fb.y, fb.z, fb.w};
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint32_t sh = (j & 1) * 16;
@@ -158,19 +185,13 @@ __global__ void __launch_bounds__(kThreads)
           hi |= byte << (8 * (j - 4));
       }
     }
-    // 4x4 byte transpose among the 4 lanes sharing tx: afterwards this lane
-    // holds, for column (tx*8 + tyl) [lo] and (tx*8 + 4 + tyl) [hi], the bytes
-    // of row pairs warp*4 + 0..3.
-    uint32_t tlo = 0, thi = 0;
+    // the transpose: byte j goes to column tx*8 + j, row pair rp
+    uint8_t *sp = &stage[sub][(tx * 8) * kColBytes + rp];
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      const uint32_t plo = __shfl_sync(0xffffffffu, lo, t * 8 + tx);
-      const uint32_t phi = __shfl_sync(0xffffffffu, hi, t * 8 + tx);
-      tlo |= byte_of(plo, tyl) << (8 * t);
-      thi |= byte_of(phi, tyl) << (8 * t);
+    for (int j = 0; j < 4; ++j) {
+      sp[j * kColBytes] = static_cast<uint8_t>(lo >> (8 * j));
+      sp[(j + 4) * kColBytes] = static_cast<uint8_t>(hi >> (8 * j));
     }
-    stage[sub][(tx * 8 + tyl) * kWordStride + warp] = tlo;
-    stage[sub][(tx * 8 + 4 + tyl) * kWordStride + warp] = thi;
   }
   __syncthreads();
 #pragma unroll
@@ -181,7 +202,7 @@ __global__ void __launch_bounds__(kThreads)
     const int64_t cg = static_cast<int64_t>(blockIdx.x) * kTileCols + c;
     const int64_t rs = row_begin + sub * kSubRows + 32 * h;
     if (cg < cols && rs < rows) {
-      const uint32_t *sp = &stage[sub][c * kWordStride + 4 * h];
+      const uint32_t *sp = reinterpret_cast<const uint32_t *>(&stage[sub][c * kColBytes + 16 * h]);
       st_stream16(codes + (cg * rows + rs) / 2, make_uint4(sp[0], sp[1], sp[2], sp[3]));
     }
   }
