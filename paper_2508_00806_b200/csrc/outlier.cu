@@ -44,9 +44,12 @@ constexpr int kSmemSumCols = 8192;           // the final CTA keeps S in shared 
 constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
 // dynamic shared memory of a launch: the stage A fold buffer, or (sum mode,
 // cols <= kSmemSumCols) the column sums + the statistics scratch for the tail
+// (rounded up to 8 KB: a handful of distinct sizes per kernel for the
+// occupancy cache below)
 static inline int col_smem(bool sum, int64_t cols) {
   const int64_t tail = (sum && cols <= kSmemSumCols) ? ((cols * 8 + 15) & ~int64_t{15}) + kStatsScratch : 0;
-  return static_cast<int>(tail > kStageASmem ? tail : (kStageASmem > kStatsScratch ? kStageASmem : kStatsScratch));
+  const int64_t need = tail > kStageASmem ? tail : (kStageASmem > kStatsScratch ? kStageASmem : kStatsScratch);
+  return static_cast<int>((need + 8191) & ~int64_t{8191});
 }
 
 // f16 half of a packed word -> f64 in one F2F.F64.F16 (reads .H0/.H1 directly;
