@@ -152,4 +152,6 @@ def profile_model(model, ops, batch_fn, *, mem_budget_bytes: int, static_mem_byt
     budget = max(int(mem_budget_bytes), static + 1)
     prof = ModelProfile(tuple(ops_out), model.cfg.n_layer, static, budget,
                         int(reference_batch), float(base_step_time_ms))
+    global _FLUSH
+    _FLUSH = None  # the 256 MB L2-flush buffer is only needed while profiling
     return prof, k_caps
