@@ -490,6 +490,33 @@ def test_outlier_decompress_one_launch_vs_two(torch_cuda, shape, group, n_hot, k
             assert torch.equal(outs[2].cpu().view(torch.uint8), ref.view(torch.uint8))
 
 
+@pytest.mark.parametrize("shape", [(777, 13), (64, 1030), (3000, 40)])
+def test_outlier_decompress_fallbacks(torch_cuda, shape):
+    """Outputs the one-launch tile kernel cannot take -- element counts not a
+    multiple of 8, an output pointer off 16-byte alignment -- fall back to the
+    dequantiser + overwrite launches with the same bytes."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200.slots import CodecSlot
+    rows, cols = shape
+    g = torch.Generator(device="cuda").manual_seed(rows * cols)
+    x = torch.randn(rows, cols, device="cuda", generator=g)
+    x[:, torch.randperm(cols, generator=g, device="cuda")[:3]] *= 60
+    x = x.to(torch.bfloat16)
+    slot = CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.OUTLIER_SEPARATED), torch.bfloat16, torch.bfloat16,
+                     k_cap=16)
+    slot.compress(x)
+    ref = slot.decompress()
+    buf = torch.empty(rows * cols + 8, dtype=torch.bfloat16, device="cuda")
+    y = buf[1:1 + rows * cols]  # 2-byte offset: not 16-byte aligned
+    slot.decompress_ptr(y.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert torch.equal(y.view(rows, cols).view(torch.int16), ref.view(torch.int16))
+    if rows * cols <= (1 << 20):
+        want, wdeq = oracle_run(x.cpu().to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+        assert torch.equal(ref.cpu().view(torch.int16), torch.from_numpy(wdeq).to(torch.bfloat16).view(torch.int16))
+
+
 @pytest.mark.parametrize("shape,dtype_name", [((512, 1024), "bfloat16"), ((1000, 40), "float32"),
                                               ((257, 4096), "float16")])
 def test_outlier_gather_modes_vs_oracle(torch_cuda, shape, dtype_name, monkeypatch):
