@@ -320,6 +320,9 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    for kv in getattr(args, "set_option", []):
+        key, val = kv.split("=", 1)
+        _lib.set_option(key, int(val))
     stream = torch.cuda.current_stream(dev)
     sptr = stream.cuda_stream
     ops = gpt_block_ops()
@@ -646,6 +649,8 @@ def main():
                     help="streams the step graph deals its independent tensors to (1 = serial; "
                          "measured 4.00 / 4.61 / 4.63 / 4.83 / 4.77 / 4.83 / 4.67 TB/s for "
                          "1 / 2 / 3 / 4 / 5 / 6 / 8)")
+    ap.add_argument("--set-option", action="append", default=[], metavar="KEY=VALUE",
+                    help="adc_set_option tuning switch for this run (results identical; repeatable)")
     ap.add_argument("--no-train", action="store_true", help="skip the training tokens/s leg")
     ap.add_argument("--train-model", default="gpt-345m")
     ap.add_argument("--train-steps", type=int, default=10)
