@@ -130,6 +130,9 @@ ADC_API unsigned long long adc_kernel_launches(void);
  *   "outlier_tile"  elements per tile of that launch: 4096, 8192 (default)
  *                   or 16384.
  *   "k4_trace"      1 = record the single-pass kernel's phase timestamps.
+ *   "sum_smem_cols" the column-statistics tail keeps the sums in shared
+ *                   memory up to this many columns (default and max 8192;
+ *                   lower = smaller CTA footprint, slower tail).
  *   "cr_trace"      1 = record the column-statistics kernel's phase
  *                   timestamps instead (adc_debug_trace_k4 then returns
  *                   those: 4 u64 per CTA, the tail's at 4096 * 4).

@@ -134,6 +134,10 @@ int adc_set_option(const char *key, int value) {
     set_k4_dbg(value);
     return ADC_OK;
   }
+  if (k == "sum_smem_cols") {  // column statistics keep the sums in shared memory up to this many columns (8192)
+    set_sum_smem_cols(value);
+    return ADC_OK;
+  }
   if (k == "cr_trace") {  // record phase timestamps of the column-statistics kernel (adc_debug_trace_k4 reads them)
     set_cr_trace(value);
     g_trace_src = value ? 1 : 0;

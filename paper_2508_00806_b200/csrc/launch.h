@@ -89,6 +89,7 @@ int launch_outlier_decompress_tiles(const Ctx &c, const uint8_t *codes, const ui
 void set_outlier_decompress_mode(int m);
 void set_outlier_tile(int t);
 void set_cr_trace(int v);
+void set_sum_smem_cols(int v);
 int read_cr_trace(unsigned long long *host, int n);
 int launch_outlier_scatter(const Ctx &c, const uint32_t *idx, const uint16_t *val,
                            const int32_t *k_dev, int64_t k_cap, int64_t rows, int64_t cols,

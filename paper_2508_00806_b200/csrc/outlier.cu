@@ -40,7 +40,8 @@ namespace adc {
 constexpr double kExactLimit = 536870912.0;  // 2^29
 constexpr int kStripCols = 256;              // 32 column units of 8 per CTA
 constexpr int kRowLanes = kThreads / 32;     // 8
-constexpr int kSmemSumCols = 8192;           // the final CTA keeps S in shared memory up to here
+constexpr int kSmemSumCols = 8192;           // the final CTA keeps S in shared memory up to here (max)
+static int g_sum_smem_cols = kSmemSumCols;   // tuning: "sum_smem_cols" lowers it
 constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
 // dynamic shared memory of a launch: the stage A fold buffer, or (sum mode,
 // cols <= kSmemSumCols) the column sums + the statistics scratch for the tail
@@ -49,7 +50,7 @@ constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
 // streams' kernels; the occupancy cache below holds 32 sizes, beyond that the
 // query simply runs per call)
 static inline int col_smem(bool sum, int64_t cols) {
-  const int64_t tail = (sum && cols <= kSmemSumCols) ? ((cols * 8 + 15) & ~int64_t{15}) + kStatsScratch : 0;
+  const int64_t tail = (sum && cols <= g_sum_smem_cols) ? ((cols * 8 + 15) & ~int64_t{15}) + kStatsScratch : 0;
   return static_cast<int>(tail > kStageASmem ? tail : (kStageASmem > kStatsScratch ? kStageASmem : kStatsScratch));
 }
 
@@ -78,6 +79,7 @@ struct ColArgs {
   double thr;
   int64_t k_cap;
   int trace;  // record phase timestamps (tuning, "cr_trace")
+  int64_t smem_cols;  // S stays in shared memory up to this many columns
   Tree tree;
   uint8_t *flag;
   uint32_t *idx;
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
   if (!s_last) return;
   CR_TRACE_TAIL(0);
   // move the accumulators out (8 columns per thread per round trip) and reset them
-  const bool s_smem = SUM && cols <= kSmemSumCols;
+  const bool s_smem = SUM && cols <= a.smem_cols;
   double *s_S = reinterpret_cast<double *>(s_buf);
   int flagged = 0;
   for (int64_t base = 0; base < cols; base += 8 * kThreads) {
@@ -324,6 +326,7 @@ __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restr
 
 static std::atomic<int> g_cr_trace{0};
 void set_cr_trace(int v) { g_cr_trace.store(v, std::memory_order_relaxed); }
+void set_sum_smem_cols(int v) { g_sum_smem_cols = v < 0 ? 0 : (v > kSmemSumCols ? kSmemSumCols : v); }
 int read_cr_trace(unsigned long long *host, int n) {
   n = n < kCrTraceCtas * 4 + 16 ? n : kCrTraceCtas * 4 + 16;
   return cudaMemcpyFromSymbol(host, g_crtrace, sizeof(unsigned long long) * n) == cudaSuccess ? n : -1;
@@ -332,6 +335,7 @@ int read_cr_trace(unsigned long long *host, int n) {
 static ColArgs make_args(int64_t rows, int64_t cols, const Workspace &ws) {
   ColArgs a{};
   a.trace = g_cr_trace.load(std::memory_order_relaxed);
+  a.smem_cols = g_sum_smem_cols;
   a.rows = rows;
   a.cols = cols;
   a.acc = ws.acc;
