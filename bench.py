@@ -239,6 +239,26 @@ def run_reference(args, rank: int) -> None:
 # ---------------------------------------------------------------------------
 # clocks sampler (NVML, polled during the timed region)
 # ---------------------------------------------------------------------------
+def gpu_local_affinity(index: int):
+    """Pin this process to the CPUs NVML reports as local to GPU `index`;
+    returns the previous affinity (None when NVML or the call is unavailable)."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(index)
+        n = max(1, ((os.cpu_count() or 64) + 63) // 64)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, n)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        prev = os.sched_getaffinity(0)
+        cpus &= prev
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+        return prev
+    except Exception:
+        return None
+
+
 class ClockSampler:
     REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
                0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -267,12 +287,15 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.002)
+            self._first.set()
+            time.sleep(0.001)
 
     def __enter__(self):
         if self.ok:
+            self._first = threading.Event()
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
+            self._first.wait(1.0)  # the sampler is running before the timed region starts
         return self
 
     def __exit__(self, *exc):
@@ -498,11 +521,19 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                           "(per_op: single-call graph replays, launch overhead included)"}
 
     # ---- e2e through the C-ABI with host buffers
-    e2e_steps = max(1, min(args.steps, 5))
+    e2e_steps = max(1, min(args.steps, 10))
+    # pinned host buffers on the GPU's own NUMA node (first touch under the
+    # GPU-local CPU affinity, restored afterwards): DMA from a remote node
+    # crosses the socket interconnect
+    prev_aff = gpu_local_affinity(local_rank) if not getattr(args, "no_numa", False) else None
     hx = [torch.empty(x.shape, dtype=x.dtype, pin_memory=True) for x in xs]
     for h, x in zip(hx, xs):
         h.copy_(x)
     hy = [torch.empty(y.shape, dtype=y.dtype, pin_memory=True) for y in outs]
+    for h in hy:
+        h.zero_()
+    if prev_aff is not None:
+        os.sched_setaffinity(0, prev_aff)
     h2d = sum(h.numel() * h.element_size() for h in hx)
     d2h = sum(h.numel() * h.element_size() for h in hy)
 
@@ -537,18 +568,24 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     e2e_step(0)
     e2e_step(1)
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for it in range(e2e_steps):
-        e2e_step(it)
-    tail = torch.cuda.Event()
-    tail.record(d2h_stream)
-    stream.wait_event(tail)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    e2e_value, _ = whole_job_rate(bytes_step * e2e_steps / 1e9, e0.elapsed_time(e1), dev)
+    # three windows of e2e_steps steps each; the median window is reported
+    # (host-side PCIe traffic varies run to run: single windows on one box
+    # measured 33-97 GB/s); every window is listed in the JSON line
+    windows = []
+    for _w in range(3):
+        if world > 1:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for it in range(e2e_steps):
+            e2e_step(it)
+        tail = torch.cuda.Event()
+        tail.record(d2h_stream)
+        stream.wait_event(tail)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        windows.append(whole_job_rate(bytes_step * e2e_steps / 1e9, e0.elapsed_time(e1), dev)[0])
+    e2e_value = statistics.median(windows)
 
     training = None
     if not args.no_train:
@@ -566,6 +603,7 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
                 "roofline": roofline, "cpu_baseline": cpu,
                 "e2e": {"value": round(e2e_value, 2), "unit": UNIT, "h2d_bytes_per_step": h2d,
                         "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+                        "windows": [round(v, 2) for v in windows], "statistic": "median of 3 windows",
                         "pipeline": "pinned H2D + eager C-ABI calls on the compute stream, D2H on a "
                                     "second stream overlapping the next step's H2D"},
                 "clocks": clocks.summary(), "gpu_launches": int(launches),
@@ -640,7 +678,7 @@ def dist_selftest(rank: int, world: int) -> None:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
@@ -651,6 +689,7 @@ def main():
                          "1 / 2 / 3 / 4 / 5 / 6 / 8)")
     ap.add_argument("--set-option", action="append", default=[], metavar="KEY=VALUE",
                     help="adc_set_option tuning switch for this run (results identical; repeatable)")
+    ap.add_argument("--no-numa", action="store_true", help="e2e: do not place pinned buffers on the GPU's node")
     ap.add_argument("--no-train", action="store_true", help="skip the training tokens/s leg")
     ap.add_argument("--train-model", default="gpt-345m")
     ap.add_argument("--train-steps", type=int, default=10)
