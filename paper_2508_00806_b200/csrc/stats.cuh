@@ -45,10 +45,12 @@ __device__ __forceinline__ int block_excl_scan(int v, int *total, int *s_tmp) {
 }
 
 // tuning timestamps of the statistics phases (null: off)
-__device__ __forceinline__ void stats_mark(unsigned long long *tm, int i) {
+__device__ __forceinline__ void stats_mark(unsigned long long *tm, int i, double dep = 0.0) {
   if (tm && threadIdx.x == 0) {
     unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    // `dep` is an input operand: the value it names is computed before the
+    // timestamp (pure arithmetic is otherwise free to move across it)
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t) : "d"(dep));
     tm[i] = t;
   }
 }
@@ -289,18 +291,22 @@ __device__ __forceinline__ int outlier_flags_block(Term<SMEM> t, double mean, do
   const int64_t c0 = min(cols, run * threadIdx.x), c1 = min(cols, c0 + run);
   int bad = 0, mine = 0, total, pos;
   if (run <= 64) {
-    // each thread owns a contiguous run of <= 64 columns: flags in a register mask
+    // each thread owns a contiguous run of <= 64 columns: flags in a register
+    // mask.  32-bit column indices (cols < 2^31 here), and the rare
+    // ambiguous column re-reads its sum instead of indexing the batch array
+    // at run time (which put the batch in local memory: 8 STL per batch)
     uint64_t bits = 0;
-    for (int64_t base = c0; base < c1; base += 8) {
+    const int i0 = static_cast<int>(c0), i1 = static_cast<int>(c1);
+    for (int base = i0; base < i1; base += 8) {
       double v[8];
 #pragma unroll
-      for (int q = 0; q < 8; ++q) v[q] = base + q < c1 ? t.load(base + q) : 0.0;
+      for (int q = 0; q < 8; ++q) v[q] = base + q < i1 ? t.load(base + q) : 0.0;
       uint32_t f8 = 0, amb = 0;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const double d = __dsub_rn(v[q], mean);
         const bool hi = d > T_hi, lo = d < T_lo;
-        const bool live = base + q < c1;
+        const bool live = base + q < i1;
         bad |= live && !(v[q] <= cap);
         f8 |= (live && hi && sigma != 0.0 ? 1u : 0u) << q;
         amb |= (live && !hi && !lo && sigma != 0.0 ? 1u : 0u) << q;
@@ -308,9 +314,9 @@ __device__ __forceinline__ int outlier_flags_block(Term<SMEM> t, double mean, do
       while (amb) {  // rare: within 2^-46 of the threshold (or NaN)
         const int q = __ffs(amb) - 1;
         amb &= amb - 1;
-        f8 |= z_exact(v[q]) << q;
+        f8 |= z_exact(t.load(base + q)) << q;
       }
-      bits |= static_cast<uint64_t>(f8) << (base - c0);
+      bits |= static_cast<uint64_t>(f8) << (base - i0);
     }
     stats_mark(tm, 2);
     bad = __syncthreads_or(bad);
@@ -420,11 +426,11 @@ __device__ __forceinline__ int outlier_stats_block(const double *S, int64_t rows
     __syncthreads();
     if (!(total < 536870912.0)) total = heap_sum(t, n, D, val);
     mean = __ddiv_rn(__dadd_rn(0.0, total), static_cast<double>(cols));
-    stats_mark(tm, 0);
+    stats_mark(tm, 0, mean);
     t.mean = mean;
     t.squared = true;
     var = __ddiv_rn(heap_sum(t, n, D, val), static_cast<double>(cols));
-    stats_mark(tm, 1);
+    stats_mark(tm, 1, var);
   } else {
     const int depth = build_tree(n, tr, s_lvl, s_tmp);
     mean = __ddiv_rn(tree_sum(t, tr, depth, s_lvl), static_cast<double>(cols));
