@@ -490,6 +490,30 @@ def test_outlier_decompress_one_launch_vs_two(torch_cuda, shape, group, n_hot, k
             assert torch.equal(outs[2].cpu().view(torch.uint8), ref.view(torch.uint8))
 
 
+@pytest.mark.parametrize("smem_cols", [0, 1024, 8192])
+@pytest.mark.parametrize("shape", [(2048, 1024), (1024, 4096), (512, 8192), (300, 16384)])
+def test_statistics_sums_in_shared_or_global_memory(torch_cuda, shape, smem_cols):
+    """The column-statistics tail gives the oracle's flags and outputs whether
+    the sums stay in shared memory or go through global memory
+    (sum_smem_cols), on the two-launch path."""
+    torch = torch_cuda
+    import paper_2508_00806_b200 as adc
+    from paper_2508_00806_b200 import _lib
+    rng = np.random.default_rng(shape[1] + smem_cols)
+    x = rng.normal(size=shape).astype(np.float32)
+    x[:, rng.choice(shape[1], max(2, shape[1] // 60), replace=False)] *= 25
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    want = oracle_run(xt.to(torch.float32).numpy(), cases.OUTL, 128, 3.0)
+    try:
+        _lib.set_option("sum_smem_cols", smem_cols)
+        _lib.set_option("outlier_path", 0)
+        got = device_run(xt, cases.OUTL, 128, 3.0)
+    finally:
+        _lib.set_option("sum_smem_cols", 8192)
+        _lib.set_option("outlier_path", 2)
+    assert cases.norm_digest(*got) == cases.norm_digest(*want)
+
+
 @pytest.mark.parametrize("shape", [(777, 13), (64, 1030), (3000, 40)])
 def test_outlier_decompress_fallbacks(torch_cuda, shape):
     """Outputs the one-launch tile kernel cannot take -- element counts not a
