@@ -49,6 +49,8 @@ constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
 // 4-stream bench step -- larger footprints co-reside less with the other
 // streams' kernels; the occupancy cache below holds 32 sizes, beyond that the
 // query simply runs per call)
+constexpr int kMaxColSmem = ((kSmemSumCols * 8 + 15) & ~15) + kStatsScratch;
+static_assert(kMaxColSmem >= kStageASmem, "attribute covers the stage A buffer");
 static inline int col_smem(bool sum, int64_t cols) {
   const int64_t tail = (sum && cols <= g_sum_smem_cols) ? ((cols * 8 + 15) & ~int64_t{15}) + kStatsScratch : 0;
   return static_cast<int>(tail > kStageASmem ? tail : (kStageASmem > kStatsScratch ? kStageASmem : kStatsScratch));
@@ -372,7 +374,9 @@ static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols, int sme
       if (cache[i].smem == smem) occ = cache[i].occ;
     }
     if (!seen)
-      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, col_smem(true, kSmemSumCols));
+      // the largest size any launch may request (independent of the runtime
+      // sum_smem_cols setting: a smaller attribute would reject later launches)
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxColSmem);
     if (occ == 0) {
       int v = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kernel, kThreads, smem);
