@@ -416,12 +416,17 @@ def run_ours(args, rank: int, world: int, local_rank: int) -> None:
     call_us = [statistics.mean(e[j].elapsed_time(e[j + 1]) for e in evs) * 1e3 for j in range(len(calls))]
     cu = {(i, ph): call_us[j] for j, (i, ph) in enumerate(calls)}
     per_op = []
+    pk, _ = measured_peak()
     for i, (op, s) in enumerate(zip(ops, slots)):
         c, d = cu[(i, "compress")], cu[(i, "decompress")]
         per_op.append({"op": op.name, "scheme": s.scheme.name, "shape": [op.rows, op.cols],
                        "k": ks[i], "compress_us": round(c, 2), "decompress_us": round(d, 2),
                        "compress_gbs": round(bytes_c[i] / c / 1e3, 1),
-                       "decompress_gbs": round(bytes_d[i] / d / 1e3, 1)})
+                       "decompress_gbs": round(bytes_d[i] / d / 1e3, 1),
+                       # fraction of the measured copy peak per call (single-call graph
+                       # replays: launch + ramp included, so small tensors read low)
+                       "compress_frac": round(bytes_c[i] / c / 1e3 / pk, 3),
+                       "decompress_frac": round(bytes_d[i] / d / 1e3 / pk, 3)})
     # With --streams S > 1 the graph forks: the tensors are dealt to S streams
     # (longest measured call pair first, greedy) and each phase (all compresses, then
     # all decompresses) joins before the next, so independent tensors' calls

@@ -27,6 +27,9 @@ bool pdl_enabled() {
   return v == 1;
 }
 void set_pdl(int v) { g_pdl.store(v ? 1 : 0, std::memory_order_relaxed); }
+static std::atomic<int> g_outlier_pdl{1};
+bool outlier_pdl_enabled() { return g_outlier_pdl.load(std::memory_order_relaxed) != 0; }
+void set_outlier_pdl(int v) { g_outlier_pdl.store(v ? 1 : 0, std::memory_order_relaxed); }
 
 void note_launches(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
 
@@ -112,6 +115,10 @@ int adc_set_option(const char *key, int value) {
   const std::string k(key);
   if (k == "pdl") {  // programmatic dependent launch on (1) / off (0, default)
     set_pdl(value);
+    return ADC_OK;
+  }
+  if (k == "outlier_pdl") {  // zeroing quantiser as a programmatic dependent of the statistics (1, default)
+    set_outlier_pdl(value);
     return ADC_OK;
   }
   if (k == "epl") {  // elements per lane of the group quantiser: 32 (default) or 16

@@ -87,7 +87,9 @@ __global__ void __launch_bounds__(kThreads)
     channel_quant(const void *__restrict__ x, int64_t rows, int64_t cols,
                   const uint32_t *__restrict__ colmax, uint8_t *__restrict__ codes,
                   uint16_t *__restrict__ scales) {
-  pdl_entry();
+  // a programmatic dependent of the column abs-max pass (launch_k_dep): the
+  // tile's rows are loaded before the wait (x is only read by that pass), the
+  // column maxima after it
   // all four sub-tiles: their rows are loaded up front (8 x 16 B in flight per
   // thread, issued before the scales are derived), quantised, and their code
   // bytes written column-major into shared memory (one byte store per column
@@ -114,6 +116,8 @@ __global__ void __launch_bounds__(kThreads)
       rb[sub].zero();
     }
   }
+  pdl_wait();
+  pdl_trigger();
 
   // Per-column quantisation constants for this thread's 8 columns.
   float qs[8], qi[8];
@@ -292,7 +296,7 @@ int launch_channel_compress(const Ctx &c, const void *x, int dt, int64_t rows, i
   dim3 gq(static_cast<unsigned>((cols + kTileCols - 1) / kTileCols),
           static_cast<unsigned>((rows + kBlockRows - 1) / kBlockRows));
   ADC_DT_SWITCH(dt, DT, {
-    launch_k(channel_quant<DT>, gq, kThreads, 0, c.stream, x, rows, cols, ws.colmax, codes, scales), note_launches(1);
+    launch_k_dep(channel_quant<DT>, gq, kThreads, 0, c.stream, x, rows, cols, ws.colmax, codes, scales), note_launches(1);
   });
   return 0;
 }

@@ -145,13 +145,51 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
                      const uint8_t *__restrict__ zflag, OutlierSide side,
                      uint32_t *__restrict__ codes, uint16_t *__restrict__ scales,
                      uint16_t *__restrict__ offsets, uint32_t *__restrict__ err) {
-  pdl_entry();
+  if (!ZERO) pdl_entry();
   constexpr int NW = EPL / 2;  // 16-bit pairs per unit
   constexpr int NC = EPL / 8;  // packed code words per unit
   using R = Raw<DT>;
   constexpr bool BF = R::kBf16;
   int64_t cta = blockIdx.x, n_ctas = gridDim.x;
+  // ZERO runs as a programmatic dependent of the column statistics
+  // (launch_k_dep): the first units of x are loaded before the wait (x is an
+  // input the statistics kernel only reads), the flags, the outlier indices
+  // and k after it
+  uint32_t wn[U][NW];
+  uint2 zfn[U][NC];
+  auto fetch_x = [&](int64_t b) {
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t u = b + k * kThreads + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < NC; ++q) {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (u < n_units) v = R::template load8<false>(x, u * EPL + 8 * q);
+        wn[k][4 * q] = v.x;
+        wn[k][4 * q + 1] = v.y;
+        wn[k][4 * q + 2] = v.z;
+        wn[k][4 * q + 3] = v.w;
+      }
+    }
+  };
+  auto fetch_flags = [&](int64_t b) {
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+      const int64_t u = b + k * kThreads + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < NC; ++q)
+        zfn[k][q] = u < n_units ? zero_flags8(u * EPL + 8 * q, dc, zflag) : make_uint2(0, 0);
+    }
+  };
+  bool pre = false;  // the first iteration's x units are in wn
   if (ZERO) {
+    const int64_t qc = cta - side.n_gather;
+    if (qc >= 0 && qc * kThreads * U < n_units_pad) {
+      fetch_x(qc * kThreads * U);
+      pre = true;
+    }
+    pdl_wait();
+    pdl_trigger();
     if (cta < side.n_gather) {
       gather_side<DT>(x, side, cta, side.n_gather);
       return;
@@ -170,27 +208,20 @@ __global__ void __launch_bounds__(kThreads, ((ASYM && EPL == 32) || EPL * U >= 6
   // before this one is processed (software pipeline), so every warp keeps a
   // unit in flight while it computes (80 registers, 3 CTAs per SM)
   constexpr bool PIPE = ASYM && EPL == 32;  // measured: asym 79.3 -> 77.5 us, sym / outlier slower
-  uint32_t wn[U][NW];
-  uint2 zfn[U][NC];
   auto fetch = [&](int64_t b) {
-#pragma unroll
-    for (int k = 0; k < U; ++k) {
-      const int64_t u = b + k * kThreads + threadIdx.x;
-#pragma unroll
-      for (int q = 0; q < NC; ++q) {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (u < n_units) v = R::template load8<false>(x, u * EPL + 8 * q);
-        wn[k][4 * q] = v.x;
-        wn[k][4 * q + 1] = v.y;
-        wn[k][4 * q + 2] = v.z;
-        wn[k][4 * q + 3] = v.w;
-        if (ZERO) zfn[k][q] = u < n_units ? zero_flags8(u * EPL + 8 * q, dc, zflag) : make_uint2(0, 0);
-      }
-    }
+    fetch_x(b);
+    if (ZERO) fetch_flags(b);
   };
   if (PIPE && cta * kThreads * U < n_units_pad) fetch(cta * kThreads * U);
   for (int64_t base = cta * kThreads * U; base < n_units_pad; base += step) {
-    if (!PIPE) fetch(base);
+    if (!PIPE) {
+      if (pre) {
+        fetch_flags(base);
+        pre = false;
+      } else {
+        fetch(base);
+      }
+    }
     uint32_t w[U][NW];
     uint2 zf[U][NC];
 #pragma unroll
@@ -781,7 +812,7 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
         launch_k(group_quant_fast<DT, true, LL, false, 32, kU32>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        launch_k(group_quant_fast<DT, false, LL, true, 32, kU32>, grid + side.n_gather, kThreads, 0, c.stream, 
+        launch_k_dep(group_quant_fast<DT, false, LL, true, 32, kU32>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
         launch_k(group_quant_fast<DT, false, LL, false, 32, kU32>, grid, kThreads, 0, c.stream, 
@@ -801,7 +832,7 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
         launch_k(group_quant_fast<DT, true, LL, false, 16, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        launch_k(group_quant_fast<DT, false, LL, true, 16, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
+        launch_k_dep(group_quant_fast<DT, false, LL, true, 16, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
         launch_k(group_quant_fast<DT, false, LL, false, 16, kUnroll>, grid, kThreads, 0, c.stream, 
@@ -821,7 +852,7 @@ int launch_group_compress(const Ctx &c, const void *x, int dt, int64_t rows, int
         launch_k(group_quant_fast<DT, true, LL, false, 8, kUnroll>, grid, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, nullptr, OutlierSide{}, codes32, scales, offsets, err), note_launches(1);
       } else if (zero) {
-        launch_k(group_quant_fast<DT, false, LL, true, 8, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
+        launch_k_dep(group_quant_fast<DT, false, LL, true, 8, kUnroll>, grid + side.n_gather, kThreads, 0, c.stream, 
             x, n_units, n_units_pad, dc, zero_flag, side, codes32, scales, nullptr, err), note_launches(1);
       } else {
         launch_k(group_quant_fast<DT, false, LL, false, 8, kUnroll>, grid, kThreads, 0, c.stream, 

@@ -47,6 +47,32 @@ inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
   cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
+// The zeroing quantiser of the outlier-separated path is launched as a
+// programmatic dependent of the column statistics (always, unless
+// adc_set_option("outlier_pdl", 0)): the statistics kernel triggers its
+// dependents once every CTA has added its column partials, so the
+// quantiser's CTAs start, and issue their first x loads (x is not written by
+// the statistics kernel), while the last statistics CTA computes mean / std /
+// flags; griddepcontrol.wait then orders every read of the flags.  The
+// per-channel quantiser follows the column abs-max pass the same way.
+bool outlier_pdl_enabled();
+void set_outlier_pdl(int v);
+template <typename... KArgs, typename... Args>
+inline void launch_k_dep(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                         Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = (pdl_enabled() || outlier_pdl_enabled()) ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 struct Ctx {
   cudaStream_t stream;
   int num_sms;

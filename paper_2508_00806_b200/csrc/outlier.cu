@@ -122,7 +122,7 @@ __device__ void numpy_order_sums(const void *x, int64_t rows, int64_t cols, doub
 
 template <int DT, bool SUM>
 __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict__ x, ColArgs a) {
-  pdl_entry();
+  pdl_wait();  // dependents are triggered after the arrival below, not here
   // stage A reduction buffer; the last CTA reuses it for S and the stats scratch
   extern __shared__ __align__(16) unsigned char s_buf[];  // col_smem(SUM, cols) bytes
   double(*red)[32][8] = reinterpret_cast<double(*)[32][8]>(s_buf);
@@ -211,6 +211,9 @@ __global__ void __launch_bounds__(kThreads, 4) colreduce(const void *__restrict_
     s_last = atom_add_acq_rel_gpu(a.done_cnt, 1u) == gridDim.x * gridDim.y - 1;
   __syncthreads();
   CR_TRACE(2);
+  // every CTA has added its partials: the zeroing quantiser (a programmatic
+  // dependent) may start loading x while the last CTA finishes the statistics
+  pdl_trigger();
   if (!s_last) return;
   CR_TRACE_TAIL(0);
   // move the accumulators out (8 columns per thread per round trip) and reset them
