@@ -130,3 +130,62 @@ def test_int4f32_device_matches_oracle(shape, group, dtype_name):
     np.testing.assert_array_equal(y.view(np.uint32), I8.dequantize_int4_f32(want).view(np.uint32))
     n = shape[0] * shape[1]
     assert ct.compressed_size_bytes == (n + 1) // 2 + 4 * -(-n // group)
+
+
+def _tie_matrix(top: float, steps: float, rows: int = 64, cols: int = 1024, seed: int = 7):
+    """Groups of 128 whose maximum is `top` and whose other elements sit on or
+    next to half-integer multiples of the scale (exact and near ties: the
+    division-free fast path must hand these to the IEEE division)."""
+    rng = np.random.default_rng(seed)
+    s = np.float32(top) / np.float32(steps)
+    k = rng.integers(-int(steps), int(steps), size=(rows, cols)).astype(np.float32)
+    x = ((k + np.float32(0.5)) * s).astype(np.float16).astype(np.float32)
+    # nudge a third of them by one f16 ulp either way
+    nudge = rng.integers(-1, 2, size=(rows, cols))
+    xb = x.astype(np.float16).view(np.uint16).astype(np.int32) + nudge
+    x = np.where(rng.random((rows, cols)) < 0.33, xb.astype(np.uint16).view(np.float16).astype(np.float32), x)
+    x[:, ::128] = top  # every group's abs-max
+    return x
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("top", [127.0, 63.5, 1.7, 3000.0, 0.011])
+def test_int8_ties_device_matches_oracle(top):
+    import torch
+    import paper_2508_00806_b200 as adc
+    x = _tie_matrix(top, 127.0)
+    want = I8.quantize_int8(x, 128)
+    ct = adc.quantize_int8(torch.from_numpy(x).cuda(), 128)
+    np.testing.assert_array_equal(ct.codes.cpu().numpy(), want.codes)
+    y = adc.dequantize_int8(ct).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), I8.dequantize_int8(want).view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("top", [8.0, 4.0, 1.7, 3000.0, 0.011])
+def test_int4f32_ties_device_matches_oracle(top):
+    import torch
+    import paper_2508_00806_b200 as adc
+    x = _tie_matrix(top, 8.0)
+    want = I8.quantize_int4_f32(x, 128)
+    ct = adc.quantize_int4_f32(torch.from_numpy(x).cuda(), 128)
+    np.testing.assert_array_equal(ct.codes.cpu().numpy(), want.codes)
+    y = adc.dequantize_int4_f32(ct).cpu().numpy()
+    np.testing.assert_array_equal(y.view(np.uint32), I8.dequantize_int4_f32(want).view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_int8_scale_division_exhaustive():
+    """The device computes RN32(top / 127) without a division: every finite
+    f16 group maximum (both signs) gives the IEEE quotient's scale and codes."""
+    import torch
+    import paper_2508_00806_b200 as adc
+    tops = np.arange(0, 0x7C00, dtype=np.uint16).view(np.float16).astype(np.float32)
+    x = np.zeros((2 * tops.size, 128), dtype=np.float32)
+    x[: tops.size, 0] = tops
+    x[tops.size:, 5] = -tops
+    x[:, 64] = x[:, 0] * 0.37 - x[:, 5] * 0.61  # one more element per group
+    want = I8.quantize_int8(x, 128)
+    ct = adc.quantize_int8(torch.from_numpy(x).cuda(), 128)
+    np.testing.assert_array_equal(ct.scales.cpu().numpy().view(np.uint32), want.scales.view(np.uint32))
+    np.testing.assert_array_equal(ct.codes.cpu().numpy(), want.codes)

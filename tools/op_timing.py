@@ -22,6 +22,11 @@ from paper_2508_00806_b200.slots import CodecSlot  # noqa: E402
 
 REPS = 20
 GRAPH = "--graph" in sys.argv
+# --opt=KEY=VALUE: adc_set_option tuning switch for this run (repeatable)
+for _a in sys.argv[1:]:
+    if _a.startswith("--opt="):
+        _k, _v = _a[len("--opt="):].split("=", 1)
+        _lib.set_option(_k, int(_v))
 
 
 def _sp():
@@ -96,6 +101,23 @@ def main():
             bc, bd = s.algorithmic_bytes(k)
             print(f"{name:12s} compress {tc:8.1f} us {bc / tc / 1e3:7.0f} GB/s | decompress {td:8.1f} us "
                   f"{bd / td / 1e3:7.0f} GB/s  (k={k})")
+        # extensions with float32 scales (int8 codes, int4 codes), g = 128
+        n = rows * cols
+        for name, fn_c, fn_d, cbytes in [("int8/f32", lib.adc_compress_int8, lib.adc_decompress_int8, n),
+                                        ("int4/f32", lib.adc_compress_int4f32, lib.adc_decompress_int4f32,
+                                         (n + 1) // 2)]:
+            bufs = [(torch.empty(cbytes, dtype=torch.uint8, device="cuda"),
+                     torch.empty(n // 128, dtype=torch.float32, device="cuda"),
+                     torch.zeros(1, dtype=torch.int32, device="cuda")) for _ in range(min(nbuf, 4))]
+            ys = [torch.empty_like(xs[0]) for _ in bufs]
+            tc = timeit([lambda sp, b=b, x=x: fn_c(x.data_ptr(), 1, rows, cols, 128, b[0].data_ptr(),
+                                                   b[1].data_ptr(), b[2].data_ptr(), sp)
+                         for b, x in zip(bufs, xs)])
+            td = timeit([lambda sp, b=b, y=y: fn_d(b[0].data_ptr(), b[1].data_ptr(), rows, cols, 128,
+                                                   y.data_ptr(), 1, sp) for b, y in zip(bufs, ys)])
+            bc = nbytes + cbytes + 4 * (n // 128)
+            print(f"{name:12s} compress {tc:8.1f} us {bc / tc / 1e3:7.0f} GB/s | decompress {td:8.1f} us "
+                  f"{bc / td / 1e3:7.0f} GB/s")
         ms = [torch.rand(rows, cols, device="cuda") < 0.9 for _ in range(min(nbuf, 4))]
         slots = [CodecSlot(rows, cols, adc.SchemeSpec(adc.Scheme.BIT_MASK, 0), torch.bool) for _ in ms]
         ys = [torch.empty((rows, cols), dtype=torch.uint8, device="cuda") for _ in ms]
