@@ -138,6 +138,10 @@ ADC_API unsigned long long adc_kernel_launches(void);
  *                   those: 4 u64 per CTA, the tail's at 4096 * 4).
  *   "k4_dbg"        timing experiments only (1 = stop the single pass after
  *                   its streaming phase; results invalid).
+ *   "outlier_pdl"   1 (default) = the zeroing / per-channel quantiser is a
+ *                   programmatic dependent launch of the column pass and
+ *                   loads its first x units while the statistics finish;
+ *                   0 = a plain stream-ordered launch.
  */
 ADC_API int adc_set_option(const char *key, int value);
 
