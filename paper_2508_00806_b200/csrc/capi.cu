@@ -121,6 +121,10 @@ int adc_set_option(const char *key, int value) {
     set_outlier_pdl(value);
     return ADC_OK;
   }
+  if (k == "cr_rows8") {  // column pass grid: 0 one full wave, 1 >= 8 rows per row lane, 2 (default) + whole batches
+    set_cr_rows8(value);
+    return ADC_OK;
+  }
   if (k == "epl") {  // elements per lane of the group quantiser: 32 (default) or 16
     set_epl(value);
     return ADC_OK;

@@ -31,6 +31,7 @@ void note_launches(int n);
 // ADC_PDL=1 / adc_set_option("pdl", 1).
 bool pdl_enabled();
 void set_pdl(int v);
+void set_cr_rows8(int v);
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                      Args... args) {

@@ -31,6 +31,7 @@
 #include "quant.cuh"
 #include "stats.cuh"
 
+#include <algorithm>
 #include <atomic>
 #include <mutex>
 #include <cstdlib>
@@ -42,6 +43,20 @@ constexpr int kStripCols = 256;              // 32 column units of 8 per CTA
 constexpr int kRowLanes = kThreads / 32;     // 8
 constexpr int kSmemSumCols = 8192;           // the final CTA keeps S in shared memory up to here (max)
 static int g_sum_smem_cols = kSmemSumCols;   // tuning: "sum_smem_cols" lowers it
+// tuning "cr_rows8" (1, the default): at least 8 rows per row lane, so a
+// short matrix runs whole batches of 8 loads in flight on fewer CTAs instead
+// of a full wave whose warps fetch their few rows one dependent load at a
+// time.  Same box: [8192,1024] column sums 10.2 -> 9.0 us, outlier-separated
+// compress 19.5 -> 18.4 us, per-channel 10.8 -> 10.0 us, bench step 4775 ->
+// 4814 GB/s; taller matrices keep the full wave (unchanged).
+// Mode 2 (the default) also shrinks the wave of a matrix with fewer than 8
+// batches per row lane until every lane's rows are whole batches of 8 (keeping
+// at least half the wave): [8192,4096] 37 -> 32 row blocks.  Same box, against
+// mode 1: [8192,4096] per-channel 31.1 -> 30.2 us, outlier-separated 48.5 ->
+// 48.1 us (two boxes), bench step 4738 -> 4843 GB/s on one box, a tie on the
+// other; applied to [131072,1024] it measured slower (column sums 46.5 ->
+// 50.3 us), hence the 8-batch bound.
+static int g_cr_rows8 = 2;
 constexpr int kStageASmem = kRowLanes * 32 * 8 * sizeof(double);
 // dynamic shared memory of a launch: the stage A fold buffer, or (sum mode,
 // cols <= kSmemSumCols) the column sums + the statistics scratch for the tail
@@ -331,6 +346,7 @@ __global__ void __launch_bounds__(kThreads) colstats_generic(const void *__restr
 
 static std::atomic<int> g_cr_trace{0};
 void set_cr_trace(int v) { g_cr_trace.store(v, std::memory_order_relaxed); }
+void set_cr_rows8(int v) { g_cr_rows8 = v == 2 ? 2 : (v ? 1 : 0); }
 void set_sum_smem_cols(int v) { g_sum_smem_cols = v < 0 ? 0 : (v > kSmemSumCols ? kSmemSumCols : v); }
 int read_cr_trace(unsigned long long *host, int n) {
   n = n < kCrTraceCtas * 4 + 16 ? n : kCrTraceCtas * 4 + 16;
@@ -389,7 +405,18 @@ static dim3 col_grid(const Ctx &c, K kernel, int64_t rows, int64_t cols, int sme
   }
   const int64_t gx = (cols + kStripCols - 1) / kStripCols;
   int64_t gy = static_cast<int64_t>(c.num_sms) * occ / gx;  // never a partial second wave
-  const int64_t maxy = (rows + kRowLanes - 1) / kRowLanes;
+  // "cr_rows8": at least 8 rows per row lane, so stage A runs whole batches of 8 loads in flight
+  const int64_t maxy = g_cr_rows8 ? std::max<int64_t>(1, rows / (8 * kRowLanes)) : (rows + kRowLanes - 1) / kRowLanes;
+  if (g_cr_rows8 == 2 && gy > 1 && rows < 64 * kRowLanes * gy) {
+    // fewer than 8 batches per row lane: make them whole -- the largest gy <= the wave with
+    // rows % (8 row lanes * 8 * gy) == 0, if it keeps at least half the wave (taller matrices
+    // keep the wave: there the remainder is a small share, and fewer CTAs measured slower)
+    for (int64_t y = std::min(gy, maxy); y >= (gy + 1) / 2 && y >= 1; --y)
+      if (rows % (8 * kRowLanes * y) == 0) {
+        gy = y;
+        break;
+      }
+  }
   if (gy > maxy) gy = maxy;
   if (gy < 1) gy = 1;
   if (gy > 65535) gy = 65535;

@@ -514,6 +514,30 @@ def test_statistics_sums_in_shared_or_global_memory(torch_cuda, shape, smem_cols
     assert cases.norm_digest(*got) == cases.norm_digest(*want)
 
 
+@pytest.mark.parametrize("rows8", [0, 1, 2])
+@pytest.mark.parametrize("shape", [(8192, 1024), (2048, 3072), (100, 4096), (131072, 64), (40, 256), (8192, 4096), (16384, 3072)])
+def test_column_pass_grid_rows8(torch_cuda, shape, rows8):
+    """The column pass's grid shape (cr_rows8: at least 8 rows per row lane)
+    changes neither the outlier-separated nor the per-channel bytes."""
+    torch = torch_cuda
+    from paper_2508_00806_b200 import _lib
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    x = rng.normal(size=shape).astype(np.float32)
+    x[:, rng.choice(shape[1], max(1, shape[1] // 90), replace=False)] *= 25
+    xt = torch.from_numpy(x).to(torch.bfloat16)
+    xf = xt.to(torch.float32).numpy()
+    try:
+        _lib.set_option("outlier_path", 0)
+        _lib.set_option("cr_rows8", rows8)
+        for scheme, g in [(cases.OUTL, 128), (cases.SYM, 0)]:
+            got = device_run(xt, scheme, g, 3.0)
+            want = oracle_run(xf, scheme, g, 3.0)
+            assert cases.norm_digest(*got) == cases.norm_digest(*want), (scheme, g)
+    finally:
+        _lib.set_option("cr_rows8", 2)
+        _lib.set_option("outlier_path", 2)
+
+
 @pytest.mark.parametrize("shape", [(777, 13), (64, 1030), (3000, 40)])
 def test_outlier_decompress_fallbacks(torch_cuda, shape):
     """Outputs the one-launch tile kernel cannot take -- element counts not a
