@@ -138,8 +138,9 @@ ADC_API unsigned long long adc_kernel_launches(void);
  *                   those: 4 u64 per CTA, the tail's at 4096 * 4).
  *   "k4_dbg"        timing experiments only (1 = stop the single pass after
  *                   its streaming phase; results invalid).
- *   "cr_rows8"      1 (default) = the column pass gives every row lane at
- *                   least 8 rows (whole batches of loads in flight); 0 = one
+ *   "cr_rows8"      2 (default) = the column pass gives every row lane at
+ *                   least 8 rows, in whole batches of 8 when a lane holds
+ *                   fewer than 8 batches; 1 = at least 8 rows only; 0 = one
  *                   full wave of CTAs whatever the row count.
  *   "outlier_pdl"   1 (default) = the zeroing / per-channel quantiser is a
  *                   programmatic dependent launch of the column pass and
